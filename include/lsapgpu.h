@@ -1,0 +1,170 @@
+/*
+ * lsapgpu.h -- C-ABI of the B200-native conflict-aware parallel DGS solver.
+ *
+ * This is the drop-in boundary for the reference's solver entry point and its
+ * step APIs (paths relative to /root/reference/proj):
+ *
+ *   lsapgpu_solve                   replaces lsap::dgs_parallel
+ *                                   (include/lsap/parallel.hpp:80, src/parallel.cpp:231-352)
+ *   lsapgpu_evaluate_all            replaces lsap::evaluate_all_parallel
+ *                                   (parallel.hpp:60-61, parallel.cpp:134-156)
+ *   lsapgpu_check_conflicts         replaces lsap::check_conflicts
+ *                                   (parallel.hpp:65, parallel.cpp:158-180)
+ *   lsapgpu_apply_parallel_switches replaces lsap::apply_parallel_switches
+ *                                   (parallel.hpp:71-74, parallel.cpp:182-229)
+ *   lsapgpu_set_matrix              replaces Instance::validate + SolverState::build_columns
+ *                                   (src/core.cpp:9-15, src/solver_state.hpp:67-76)
+ *   lsapgpu_random_perm / lsapgpu_objective
+ *                                   host helpers equal to lsap::random_perm (include/lsap/rng.hpp:37-46)
+ *                                   and lsap::objective (src/core.cpp:17-24)
+ *
+ * Plain pointers and sizes only.  Host buffers stay owned by the caller; the
+ * context owns all device memory, streams and the cached CUDA graph.  One
+ * context per host thread; contexts on different devices may run
+ * concurrently.  Every call returns LSAPGPU_OK or an error code, with the
+ * message (worded like the reference's lsap::Error, types.hpp:17-20) available
+ * from lsapgpu_last_error().  There is no CPU fallback: without a usable
+ * sm_100 device lsapgpu_create fails.
+ */
+#ifndef LSAPGPU_H
+#define LSAPGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSAPGPU_OK 0
+#define LSAPGPU_ERR_INVALID 1  /* lsap::Error: invalid instance / config / arguments */
+#define LSAPGPU_ERR_CUDA 2     /* CUDA runtime failure (no device, OOM, launch error) */
+#define LSAPGPU_ERR_INTERNAL 3 /* "internal: conflict check admitted overlapping exchanges" */
+#define LSAPGPU_ERR_STATE 4    /* call order (e.g. solve before set_matrix) */
+
+/* element type of a caller's matrix buffer */
+#define LSAPGPU_F64 0
+#define LSAPGPU_F32 1
+#define LSAPGPU_I32 2
+#define LSAPGPU_I16 3
+
+/* device storage chosen by set_matrix (narrowest lossless) */
+#define LSAPGPU_STORE_I16 0
+#define LSAPGPU_STORE_I32 1
+#define LSAPGPU_STORE_F32 2
+#define LSAPGPU_STORE_F64 3
+
+/* on-device synthetic instances (geom.cpp:15-33) */
+#define LSAPGPU_GEN_UNIFORM_INT 1 /* (double)(next() % param) */
+#define LSAPGPU_GEN_UNIT_F32 2    /* (double)(float)unit_double(next()) */
+#define LSAPGPU_GEN_UNIT_SCALED 3 /* unit_double(next()) * param */
+#define LSAPGPU_GEN_P2P 4         /* P2P-streaming shaped integers */
+#define LSAPGPU_GEN_GEOM 5        /* Euclidean distances, bound = param */
+
+/* ParallelConfig::Reeval (parallel.hpp:21-22) */
+#define LSAPGPU_REEVAL_TOUCHED_AND_CONFLICTED 0
+#define LSAPGPU_REEVAL_TOUCHED_ONLY 1
+
+typedef struct lsapgpu_ctx lsapgpu_ctx;
+
+typedef struct {
+  uint64_t seed;              /* DgsConfig::seed (dgs.hpp:11) */
+  double eps;                 /* DgsConfig::improvement_epsilon (dgs.hpp:15) */
+  int32_t reeval;             /* LSAPGPU_REEVAL_* */
+  int32_t use_graph;          /* 1: inner loop as one CUDA-graph launch (default); 0: host-stepped */
+  int64_t deadline_ns;        /* DgsConfig::deadline; < 0 = none */
+  const int32_t* init_sigma;  /* optional initial sigma (job -> agent); NULL = random_perm(seed) */
+} lsapgpu_params;
+
+typedef struct {
+  int64_t outer_iterations;   /* SolveReport::outer_iterations */
+  int64_t switches_applied;   /* SolveReport::switches_applied */
+  int32_t terminated_by;      /* 0 converged, 1 deadline (SolveReport::terminated_by) */
+  double value;               /* SolveReport::assignment.value (ordered objective) */
+  double elapsed_ms;          /* SolveReport::elapsed */
+  /* instrumentation (not in SolveReport) */
+  int64_t inner_iterations;   /* conflict-check batches */
+  int64_t pair_items;         /* (agent, tau[agent]) rows scanned: full sweeps + re-evaluation */
+  int64_t agent_scans;
+  int64_t job_scans;
+  int64_t lfmm_rounds;
+  int64_t scan_launches;
+  int64_t bytes_scanned;      /* algorithmic HBM bytes of the pair scans: pair_items * 2 * n * elem */
+  int32_t storage;            /* LSAPGPU_STORE_* */
+  int32_t pad_;
+} lsapgpu_stats;
+
+const char* lsapgpu_version(void);
+int lsapgpu_device_count(void);
+
+int lsapgpu_create(lsapgpu_ctx** out, int device);
+void lsapgpu_destroy(lsapgpu_ctx* ctx);
+const char* lsapgpu_last_error(const lsapgpu_ctx* ctx);
+/* the stream all work of this context is ordered on (a cudaStream_t) */
+void* lsapgpu_stream(lsapgpu_ctx* ctx);
+
+/* Instance upload.  `data` is a row-major n x n matrix of `dtype` in host
+ * memory (pinned or pageable).  Validates n >= 1 and finiteness exactly like
+ * Instance::validate, chooses the narrowest lossless device storage, and
+ * builds A and AT in HBM. */
+int lsapgpu_set_matrix(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype);
+/* Same, for a matrix already in device memory of this context's device. */
+int lsapgpu_set_matrix_device(lsapgpu_ctx* ctx, const void* dev_data, int32_t n, int32_t dtype);
+/* Synthetic instance generated on the device (LSAPGPU_GEN_*). */
+int lsapgpu_generate(lsapgpu_ctx* ctx, int32_t kind, int32_t n, uint64_t seed, double param);
+int32_t lsapgpu_n(const lsapgpu_ctx* ctx);
+int32_t lsapgpu_storage(const lsapgpu_ctx* ctx);
+/* Copy rows of the (device) instance back as fp64, row-major nrows x n. */
+int lsapgpu_read_rows(lsapgpu_ctx* ctx, const int32_t* rows, int32_t nrows, double* out);
+
+/* lsap::dgs_parallel.  sigma_out / tau_out: n entries each (tau_out may be
+ * NULL).  trace_switch / trace_value may be NULL; otherwise they receive up to
+ * trace_cap entries of SolveReport::objective_trace and *trace_len its full
+ * length. */
+int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma_out,
+                  int32_t* tau_out, lsapgpu_stats* stats, int64_t* trace_switch,
+                  double* trace_value, int64_t trace_cap, int64_t* trace_len);
+
+/* lsap::evaluate_all_parallel: SoA records; partner -1 = inactive (delta 0). */
+int lsapgpu_evaluate_all(lsapgpu_ctx* ctx, const int32_t* sigma, double eps, double* agent_delta,
+                         int32_t* agent_partner, double* job_delta, int32_t* job_partner);
+
+/* lsap::check_conflicts.  Inputs: tables with inactive deltas already 0 (the
+ * normalisation check_conflicts applies, parallel.cpp:166-173) and sigma.
+ * Outputs u8[n] masks and the ascending conflicted_jobs list (returns its
+ * length through *n_conflicted_jobs).  Needs no matrix; n is given. */
+int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_delta,
+                            const int32_t* agent_partner, const double* job_delta,
+                            const int32_t* job_partner, const int32_t* sigma,
+                            uint8_t* agent_accepted, uint8_t* job_accepted,
+                            uint8_t* reserved_mask, uint8_t* conflicted_mask,
+                            int32_t* conflicted_jobs, int32_t* n_conflicted_jobs);
+
+/* lsap::apply_parallel_switches on the context's matrix.  sigma/tau/value are
+ * updated in place; applied_* (n entries each) receive the applied exchanges
+ * in commit order; returns the count through *n_applied. */
+int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* tau, double* value,
+                                    const double* agent_delta, const int32_t* agent_partner,
+                                    const uint8_t* agent_active, const double* job_delta,
+                                    const int32_t* job_partner, const uint8_t* job_active,
+                                    const uint8_t* agent_accepted, const uint8_t* job_accepted,
+                                    double eps, int32_t* applied_agent, int32_t* applied_new_job,
+                                    int32_t* applied_old_job, int32_t* applied_displaced,
+                                    double* applied_delta, int32_t* n_applied);
+
+/* Host helpers (sequential by nature; identical to the reference's). */
+void lsapgpu_random_perm(int32_t n, uint64_t seed, int32_t* out);
+int lsapgpu_objective(lsapgpu_ctx* ctx, const int32_t* sigma, double* value);
+
+/* Instrumented re-run support for bench.py: time every pair-scan launch of
+ * the last host-stepped solve with CUDA events on the launching stream.
+ * Returns the summed scan time (ms) and launch count of the last solve that
+ * ran with use_graph = 0 and timing enabled. */
+int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled);
+int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
+                        double* full_sweep_ms, int64_t* full_sweeps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSAPGPU_H */

@@ -1,0 +1,253 @@
+// layout.cu -- device-resident instance layout (replaces Instance::validate,
+// proj/src/core.cpp:9-15, and SolverState::build_columns,
+// proj/src/solver_state.hpp:67-76), on-device synthetic instance generators
+// (geom.cpp:15-33), and the O(n) assignment helpers.
+//
+// classify: one pass over the fp64 (or narrower) source that decides the
+//   narrowest lossless storage type and detects non-finite entries.
+// build_layout: 32x32 smem-tiled convert + transpose writing A and AT in one
+//   pass (read 1x, write 2x).  The generators plug in as the tile source, so a
+//   100k x 100k instance never exists in host memory or as an fp64 copy.
+#include <cmath>
+
+#include "state.h"
+
+namespace lsapgpu {
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// k-th draw of SplitMix64(seed) (rng.hpp:11-22): counter-based.
+__device__ __forceinline__ uint64_t draw(uint64_t seed, uint64_t k) {
+  return mix64(seed + (k + 1) * 0x9E3779B97F4A7C15ull);
+}
+// rng.hpp:32-34: u / (2^64 - 1); the divisor rounds to 2^64 in fp64.
+__device__ __forceinline__ double unit_double(uint64_t u) {
+  return __ddiv_rn(__ull2double_rn(u), 18446744073709551615.0);
+}
+
+struct Src {
+  LayoutSource s;
+  int32_t n;
+  __device__ __forceinline__ double operator()(int64_t i, int64_t j) const {
+    const int64_t k = i * n + j;
+    switch (s.kind) {
+      case 0:
+        switch (s.src_dtype) {
+          case 0: return static_cast<const double*>(s.src)[k];
+          case 1: return static_cast<double>(static_cast<const float*>(s.src)[k]);
+          case 2: return static_cast<double>(static_cast<const int32_t*>(s.src)[k]);
+          default: return static_cast<double>(static_cast<const int16_t*>(s.src)[k]);
+        }
+      case 1:
+        return __ull2double_rn(draw(s.seed, static_cast<uint64_t>(k)) %
+                               static_cast<uint64_t>(s.param));
+      case 2:
+        return static_cast<double>(__double2float_rn(unit_double(draw(s.seed, static_cast<uint64_t>(k)))));
+      case 3:
+        return __dmul_rn(unit_double(draw(s.seed, static_cast<uint64_t>(k))), s.param);
+      case 4: {  // p2p: aux = up[n], x[n], y[n]
+        if (i == j) return 0.0;
+        const double* up = s.aux;
+        const double* xs = s.aux + n;
+        const double* ys = s.aux + 2 * static_cast<int64_t>(n);
+        const int64_t dx = llabs(static_cast<int64_t>(xs[i]) - static_cast<int64_t>(xs[j]));
+        const int64_t dy = llabs(static_cast<int64_t>(ys[i]) - static_cast<int64_t>(ys[j]));
+        const int64_t lat = 1 + (dx + dy) / 16;
+        return static_cast<double>(static_cast<int64_t>(up[i]) * (256 - lat));
+      }
+      default: {  // geom: aux = xs[n], ys[n]
+        const double dx = __dsub_rn(s.aux[i], s.aux[j]);
+        const double dy = __dsub_rn(s.aux[n + i], s.aux[n + j]);
+        return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+      }
+    }
+  }
+};
+
+__global__ void gen_aux_kernel(LayoutSource s, int32_t n, double* aux) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (s.kind == 4) {
+    aux[k] = static_cast<double>(1ll << (draw(s.seed, static_cast<uint64_t>(k)) % 6));
+    aux[n + k] = static_cast<double>(draw(s.seed, static_cast<uint64_t>(n) + 2ull * k) % 1024);
+    aux[2 * static_cast<int64_t>(n) + k] =
+        static_cast<double>(draw(s.seed, static_cast<uint64_t>(n) + 2ull * k + 1) % 1024);
+  } else if (s.kind == 5) {
+    aux[k] = __dmul_rn(unit_double(draw(s.seed, 2ull * k)), s.param);
+    aux[n + k] = __dmul_rn(unit_double(draw(s.seed, 2ull * k + 1)), s.param);
+  }
+}
+
+__global__ void classify_kernel(Src src, int64_t row0, int64_t rows, uint32_t* flags) {
+  const int64_t total = rows * src.n;
+  uint32_t f = 0;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = row0 + k / src.n, j = k % src.n;
+    const double v = src(i, j);
+    if (!isfinite(v)) {
+      f |= 1u | 2u | 4u | 8u;
+      continue;
+    }
+    const bool integral = v == trunc(v);
+    if (!(integral && fabs(v) <= 32767.0)) f |= 2u;
+    if (!(integral && fabs(v) < 536870912.0)) f |= 4u;
+    if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
+  }
+  // warp then block OR, one atomic per block
+  for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
+  __shared__ uint32_t wf[32];
+  if ((threadIdx.x & 31) == 0) wf[threadIdx.x >> 5] = f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) r |= wf[w];
+    if (r) atomicOr(flags, r);
+  }
+}
+
+template <class E>
+__device__ __forceinline__ E narrow(double v) {
+  if constexpr (sizeof(E) == 2)
+    return static_cast<int16_t>(__double2int_rn(v));
+  else if constexpr (Traits<E>::kInt)
+    return static_cast<int32_t>(__double2int_rn(v));
+  else if constexpr (sizeof(E) == 4)
+    return __double2float_rn(v);
+  else
+    return v;
+}
+
+// 32x32 tiles, 32x8 threads: A tile written row-major, AT tile through smem.
+template <class E>
+__global__ void build_layout_kernel(Src src, int64_t row0, int64_t rows, E* A, E* AT, int64_t ld) {
+  __shared__ E tile[32][33];
+  const int64_t bi = row0 + static_cast<int64_t>(blockIdx.y) * 32;  // agent block
+  const int64_t bj = static_cast<int64_t>(blockIdx.x) * 32;         // job block
+  const int n = src.n;
+  const int64_t rend = row0 + rows;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = bi + r, j = bj + threadIdx.x;
+    if (i < rend && j < n) {
+      const E v = narrow<E>(src(i, j));
+      A[i * ld + j] = v;
+      tile[r][threadIdx.x] = v;
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = bj + r, i = bi + threadIdx.x;
+    if (j < n && i < rend) AT[j * ld + i] = tile[threadIdx.x][r];
+  }
+}
+
+template <class E>
+__global__ void init_assignment_kernel(DevState d) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.n) return;
+  const E* A = static_cast<const E*>(d.A);
+  const int32_t i = d.sigma[j];
+  d.tau[i] = j;
+  static_cast<E*>(d.acur)[i] = A[static_cast<int64_t>(i) * d.ld + j];
+}
+
+template <class E>
+__global__ void gather_current_kernel(DevState d, double* out) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.n) return;
+  const E* A = static_cast<const E*>(d.A);
+  out[j] = static_cast<double>(A[static_cast<int64_t>(d.sigma[j]) * d.ld + j]);
+}
+
+template <class E>
+__global__ void read_rows_kernel(DevState d, const int32_t* rows, int32_t nrows, double* out) {
+  const E* A = static_cast<const E*>(d.A);
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       k < static_cast<int64_t>(nrows) * d.n; k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = k / d.n, j = k % d.n;
+    out[k] = static_cast<double>(A[static_cast<int64_t>(rows[r]) * d.ld + j]);
+  }
+}
+
+template <template <class> class K, class... Args>
+cudaError_t dispatch(int storage, dim3 g, dim3 b, cudaStream_t st, Args... args) {
+  switch (storage) {
+    case kI16: K<int16_t>::run(g, b, st, args...); break;
+    case kI32: K<int32_t>::run(g, b, st, args...); break;
+    case kF32: K<float>::run(g, b, st, args...); break;
+    case kF64: K<double>::run(g, b, st, args...); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <class E>
+struct BuildK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, Src s, int64_t r0, int64_t rows, void* A, void* AT,
+                  int64_t ld) {
+    build_layout_kernel<E><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld);
+  }
+};
+template <class E>
+struct InitK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, DevState d) {
+    init_assignment_kernel<E><<<g, b, 0, st>>>(d);
+  }
+};
+template <class E>
+struct GatherK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, DevState d, double* out) {
+    gather_current_kernel<E><<<g, b, 0, st>>>(d, out);
+  }
+};
+template <class E>
+struct RowsK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, DevState d, const int32_t* rows, int32_t nr,
+                  double* out) {
+    read_rows_kernel<E><<<g, b, 0, st>>>(d, rows, nr, out);
+  }
+};
+
+}  // namespace
+
+cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaStream_t st) {
+  gen_aux_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, n, aux);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_classify(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
+                            uint32_t* flags, cudaStream_t st) {
+  Src src{s, n};
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  classify_kernel<<<sms * 8, 256, 0, st>>>(src, row0, rows, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
+                                int storage, void* A, void* AT, int64_t ld, cudaStream_t st) {
+  Src src{s, n};
+  dim3 g(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  return dispatch<BuildK>(storage, g, dim3(32, 8), st, src, row0, rows, A, AT, ld);
+}
+
+cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st) {
+  return dispatch<InitK>(d.storage, dim3((d.n + 255) / 256), dim3(256), st, d);
+}
+
+cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st) {
+  return dispatch<GatherK>(d.storage, dim3((d.n + 255) / 256), dim3(256), st, d, out);
+}
+
+cudaError_t launch_read_rows(const DevState& d, const int32_t* rows, int32_t nrows, double* out,
+                             cudaStream_t st) {
+  return dispatch<RowsK>(d.storage, dim3(1024), dim3(256), st, d, rows, nrows, out);
+}
+
+}  // namespace lsapgpu

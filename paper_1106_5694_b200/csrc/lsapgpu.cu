@@ -1,0 +1,832 @@
+// lsapgpu.cu -- host orchestration behind the C-ABI (include/lsapgpu.h).
+//
+// The outer loop of lsap::dgs_parallel (proj/src/parallel.cpp:255-346) runs on
+// the host, once per full pass: a full pair-scan sweep, then the whole inner
+// batch loop as ONE launch of a CUDA graph whose conditional WHILE node
+// repeats {commit kernel, pair-scan kernel} until the commit kernel finds no
+// active record (the argmax continue test, parallel.cpp:265-267) and clears
+// the graph condition on the device.  The host syncs once per outer pass to
+// drain the delta log, which it replays in the reference's batch order to
+// reproduce SolveReport::objective_trace and the exact `value == f_start`
+// termination test (parallel.cpp:306-310, 343-345).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lsapgpu.h"
+#include "state.h"
+
+using namespace lsapgpu;
+
+namespace {
+
+constexpr int64_t kTraceCap = 100000;  // parallel.cpp:15
+
+size_t esize(int storage) {
+  switch (storage) {
+    case kI16: return 2;
+    case kI32: return 4;
+    case kF32: return 4;
+    default: return 8;
+  }
+}
+size_t src_size(int dtype) {
+  switch (dtype) {
+    case LSAPGPU_F64: return 8;
+    case LSAPGPU_F32: return 4;
+    case LSAPGPU_I32: return 4;
+    default: return 2;
+  }
+}
+
+__global__ void set_deadline_kernel(Ctrl* c, int64_t remaining_ns) {
+  c->expired = 0;
+  c->error = 0;
+  c->deadline_gt = remaining_ns < 0 ? 0ull : globaltimer() + static_cast<uint64_t>(remaining_ns);
+}
+
+// Start of an outer pass (or of a resumed inner loop after a log drain).
+__global__ void begin_pass_kernel(Ctrl* c, int full) {
+  if (full) {
+    c->edge_count[0] = 0;
+    c->edge_count[1] = 0;
+  }
+  c->inner_done = 0;
+  c->drain = 0;
+  c->log_count = 0;
+}
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct lsapgpu_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  DevState d;
+  int32_t n_vec = 0;      // vectors allocated for this n
+  int32_t n_matrix = 0;   // matrix present for this n (0 = none)
+  std::vector<Buf> vec_bufs;
+  Buf mat;                // A and AT (one allocation)
+  Ctrl* ctrl_dev = nullptr;
+  Ctrl* ctrl_host = nullptr;  // pinned mirror
+  uint32_t* flags_dev = nullptr;
+
+  ScanPlan scan_plan;
+  CommitPlan commit_plan;
+
+  // cached inner-loop graph
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  double graph_eps = -1.0;
+  int graph_policy = -1;
+
+  // scan timing (host-stepped mode)
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double scan_ms = 0.0, full_ms = 0.0;
+  int64_t scan_launches = 0, full_launches = 0;
+};
+
+namespace {
+
+int fail(lsapgpu_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, LSAPGPU_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+void drop_graph(lsapgpu_ctx* ctx) {
+  if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  ctx->exec = nullptr;
+  ctx->graph = nullptr;
+}
+
+void free_vectors(lsapgpu_ctx* ctx) {
+  for (auto& b : ctx->vec_bufs) cudaFree(b.p);
+  ctx->vec_bufs.clear();
+  ctx->n_vec = 0;
+}
+
+template <class T>
+cudaError_t valloc(lsapgpu_ctx* ctx, T** p, size_t count, bool zero) {
+  void* q = nullptr;
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) return e;
+  if (zero) {
+    e = cudaMemsetAsync(q, 0, bytes, ctx->stream);
+    if (e != cudaSuccess) return e;
+  }
+  ctx->vec_bufs.push_back({q, bytes});
+  *p = static_cast<T*>(q);
+  return cudaSuccess;
+}
+
+int64_t pitch_of(int32_t n) { return (static_cast<int64_t>(n) + 63) / 64 * 64; }
+
+// Per-n vectors (everything except the matrix).
+int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
+  if (ctx->n_vec == n) return LSAPGPU_OK;
+  drop_graph(ctx);
+  free_vectors(ctx);
+  DevState& d = ctx->d;
+  const int64_t ld = pitch_of(n);
+  const size_t N = static_cast<size_t>(ld), N2 = 2 * N;
+  d.n = n;
+  d.ld = ld;
+  CK(valloc(ctx, &d.sigma, N, true));
+  CK(valloc(ctx, &d.tau, N, true));
+  void* acur = nullptr;
+  CK(valloc(ctx, reinterpret_cast<double**>(&acur), N, true));  // 8 bytes/elem covers any storage
+  d.acur = acur;
+  CK(valloc(ctx, &d.agent_delta, N, true));
+  CK(valloc(ctx, &d.agent_partner, N, true));
+  CK(valloc(ctx, &d.job_delta, N, true));
+  CK(valloc(ctx, &d.job_partner, N, true));
+  CK(valloc(ctx, &d.edges[0], N2, false));
+  CK(valloc(ctx, &d.edges[1], N2, false));
+  CK(valloc(ctx, &d.eu, N2, false));
+  CK(valloc(ctx, &d.ev, N2, false));
+  CK(valloc(ctx, &d.eprop, N2, false));
+  CK(valloc(ctx, &d.estate, N2, false));
+  CK(valloc(ctx, &d.c_jnew, N2, false));
+  CK(valloc(ctx, &d.c_delta, N2, false));
+  CK(valloc(ctx, &d.keys, N, true));
+  CK(valloc(ctx, &d.touched_stamp, N, true));
+  CK(valloc(ctx, &d.conf_stamp, N, true));
+  CK(valloc(ctx, &d.rej_stamp, N2, true));
+  CK(valloc(ctx, &d.items, N, false));
+  d.log_cap = std::max<int64_t>(1 << 20, 8 * static_cast<int64_t>(n));
+  CK(valloc(ctx, &d.log, static_cast<size_t>(d.log_cap), false));
+  d.part_cap = (static_cast<int64_t>(n) + 8) * 16;
+  CK(valloc(ctx, &d.part_ad, static_cast<size_t>(d.part_cap), false));
+  CK(valloc(ctx, &d.part_at, static_cast<size_t>(d.part_cap), false));
+  CK(valloc(ctx, &d.part_jd, static_cast<size_t>(d.part_cap), false));
+  CK(valloc(ctx, &d.part_ji, static_cast<size_t>(d.part_cap), false));
+  CK(valloc(ctx, &d.part_arrive, N + 8, true));
+  d.ctrl = ctx->ctrl_dev;
+  ctx->n_vec = n;
+  // Key epochs and iteration stamps restart with fresh (zeroed) vectors.
+  std::memset(ctx->ctrl_host, 0, sizeof(Ctrl));
+  ctx->ctrl_host->round = 1;
+  CK(cudaMemcpyAsync(ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return LSAPGPU_OK;
+}
+
+int pull_ctrl(lsapgpu_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return LSAPGPU_OK;
+}
+int push_ctrl(lsapgpu_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  return LSAPGPU_OK;
+}
+
+// Builds A/AT from a layout source; src_rows_dev is a device pointer for memory sources.
+int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
+  int rc = ensure_vectors(ctx, n);
+  if (rc) return rc;
+  ctx->n_matrix = 0;
+  drop_graph(ctx);
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(uint32_t), ctx->stream));
+  CK(launch_classify(src, n, 0, n, ctx->flags_dev, ctx->stream));
+  uint32_t flags = 0;
+  CK(cudaMemcpyAsync(&flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+  int storage = kF64;
+  if (!(flags & 2u))
+    storage = kI16;
+  else if (!(flags & 4u))
+    storage = kI32;
+  else if (!(flags & 8u))
+    storage = kF32;
+  const int64_t ld = pitch_of(n);
+  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(ld) * esize(storage);
+  if (ctx->mat.bytes < 2 * bytes) {
+    if (ctx->mat.p) cudaFree(ctx->mat.p);
+    ctx->mat.p = nullptr;
+    ctx->mat.bytes = 0;
+    CK(cudaMalloc(&ctx->mat.p, 2 * bytes));
+    ctx->mat.bytes = 2 * bytes;
+  }
+  DevState& d = ctx->d;
+  d.storage = storage;
+  d.A = ctx->mat.p;
+  d.AT = static_cast<unsigned char*>(ctx->mat.p) + bytes;
+  CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), ld,
+                         ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->scan_plan = plan_scan(d, ctx->num_sms);
+  ctx->commit_plan = plan_commit(d);
+  ctx->n_matrix = n;
+  return LSAPGPU_OK;
+}
+
+bool is_perm(const int32_t* p, int32_t n) {
+  std::vector<uint8_t> seen(n, 0);
+  for (int32_t k = 0; k < n; ++k) {
+    if (p[k] < 0 || p[k] >= n || seen[p[k]]) return false;
+    seen[p[k]] = 1;
+  }
+  return true;
+}
+
+// Ordered objective (core.cpp:17-24) over the device matrix and a device sigma.
+int device_objective(lsapgpu_ctx* ctx, double* value) {
+  const int32_t n = ctx->d.n;
+  double* dv = reinterpret_cast<double*>(ctx->d.c_delta);  // scratch (2n doubles)
+  CK(launch_gather_current(ctx->d, dv, ctx->stream));
+  std::vector<double> hv(n);
+  CK(cudaMemcpyAsync(hv.data(), dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double sum = 0.0;
+  for (int32_t j = 0; j < n; ++j) sum += hv[j];
+  *value = sum;
+  return LSAPGPU_OK;
+}
+
+int build_graph(lsapgpu_ctx* ctx) {
+  drop_graph(ctx);
+  CK(cudaGraphCreate(&ctx->graph, 0));
+  cudaGraphConditionalHandle cond;
+  CK(cudaGraphConditionalHandleCreate(&cond, ctx->graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = cond;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, ctx->graph, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  cudaError_t e1 = launch_commit(ctx->d, ctx->commit_plan, kCommitSolve, cond, 1, ctx->stream);
+  cudaError_t e2 = launch_scan(ctx->d, ctx->scan_plan, 0, ctx->stream);
+  cudaGraph_t captured = body;
+  CK(cudaStreamEndCapture(ctx->stream, &captured));
+  CK(e1);
+  CK(e2);
+  CK(cudaGraphInstantiate(&ctx->exec, ctx->graph, 0));
+  ctx->graph_eps = ctx->d.eps;
+  ctx->graph_policy = ctx->d.policy;
+  return LSAPGPU_OK;
+}
+
+int run_scan(lsapgpu_ctx* ctx, int full) {
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  CK(launch_scan(ctx->d, ctx->scan_plan, full, ctx->stream));
+  if (ctx->timing) {
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->scan_ms += ms;
+    ++ctx->scan_launches;
+    if (full) {
+      ctx->full_ms += ms;
+      ++ctx->full_launches;
+    }
+  }
+  return LSAPGPU_OK;
+}
+
+struct TraceSink {
+  int64_t* ts;
+  double* tv;
+  int64_t cap;
+  int64_t len = 0;
+  void push(int64_t sw, double v, bool force = false) {
+    if (!force && len >= kTraceCap) return;
+    if (ts && tv && len < cap) {
+      ts[len] = sw;
+      tv[len] = v;
+    }
+    ++len;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* lsapgpu_version(void) { return "paper_1106_5694_b200 lsapgpu 0.1 (sm_100a)"; }
+
+int lsapgpu_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int lsapgpu_create(lsapgpu_ctx** out, int device) {
+  if (!out) return LSAPGPU_ERR_INVALID;
+  *out = nullptr;
+  auto* ctx = new lsapgpu_ctx();
+  ctx->device = device;
+  int major = 0;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) {
+    delete ctx;
+    return LSAPGPU_ERR_CUDA;
+  }
+  if (major < 10) {
+    delete ctx;
+    return LSAPGPU_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
+      cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||
+      cudaMalloc(&ctx->flags_dev, sizeof(uint32_t)) != cudaSuccess ||
+      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+    lsapgpu_destroy(ctx);
+    return LSAPGPU_ERR_CUDA;
+  }
+  std::memset(ctx->ctrl_host, 0, sizeof(Ctrl));
+  ctx->ctrl_host->round = 1;
+  cudaMemcpy(ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice);
+  *out = ctx;
+  return LSAPGPU_OK;
+}
+
+void lsapgpu_destroy(lsapgpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  drop_graph(ctx);
+  free_vectors(ctx);
+  if (ctx->mat.p) cudaFree(ctx->mat.p);
+  if (ctx->ctrl_dev) cudaFree(ctx->ctrl_dev);
+  if (ctx->ctrl_host) cudaFreeHost(ctx->ctrl_host);
+  if (ctx->flags_dev) cudaFree(ctx->flags_dev);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* lsapgpu_last_error(const lsapgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* lsapgpu_stream(lsapgpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int32_t lsapgpu_n(const lsapgpu_ctx* ctx) { return ctx ? ctx->n_matrix : 0; }
+int32_t lsapgpu_storage(const lsapgpu_ctx* ctx) { return ctx && ctx->n_matrix ? ctx->d.storage : -1; }
+
+int lsapgpu_set_matrix_device(lsapgpu_ctx* ctx, const void* dev_data, int32_t n, int32_t dtype) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
+  if (dtype < 0 || dtype > 3) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown matrix dtype");
+  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  LayoutSource s;
+  s.kind = 0;
+  s.src = dev_data;
+  s.src_dtype = dtype;
+  return build_from_source(ctx, s, n);
+}
+
+int lsapgpu_set_matrix(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
+  if (dtype < 0 || dtype > 3) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown matrix dtype");
+  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(n) * src_size(dtype);
+  void* stage = nullptr;
+  CK(cudaMalloc(&stage, bytes));
+  cudaError_t e = cudaMemcpyAsync(stage, data, bytes, cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(stage);
+    return fail(ctx, LSAPGPU_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
+  }
+  const int rc = lsapgpu_set_matrix_device(ctx, stage, n, dtype);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(stage);
+  return rc;
+}
+
+int lsapgpu_generate(lsapgpu_ctx* ctx, int32_t kind, int32_t n, uint64_t seed, double param) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
+  if (kind < 1 || kind > 5) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown generator kind");
+  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  if (kind == LSAPGPU_GEN_UNIFORM_INT && !(param >= 1.0))
+    return fail(ctx, LSAPGPU_ERR_INVALID, "uniform int modulus must be >= 1");
+  if (kind == LSAPGPU_GEN_GEOM && !(param > 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "geom: bound must be > 0");
+  double* aux = nullptr;
+  CK(cudaMalloc(&aux, sizeof(double) * 3 * static_cast<size_t>(n)));
+  LayoutSource s;
+  s.kind = kind;
+  s.seed = seed;
+  s.param = param;
+  s.aux = aux;
+  cudaError_t e = launch_gen_aux(s, n, aux, ctx->stream);
+  int rc = e == cudaSuccess ? build_from_source(ctx, s, n)
+                            : fail(ctx, LSAPGPU_ERR_CUDA, cudaGetErrorString(e));
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(aux);
+  return rc;
+}
+
+int lsapgpu_read_rows(lsapgpu_ctx* ctx, const int32_t* rows, int32_t nrows, double* out) {
+  if (!ctx || !ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  CK(cudaSetDevice(ctx->device));
+  const int32_t n = ctx->n_matrix;
+  for (int32_t r = 0; r < nrows; ++r)
+    if (rows[r] < 0 || rows[r] >= n) return fail(ctx, LSAPGPU_ERR_INVALID, "row index out of range");
+  int32_t* drows = nullptr;
+  double* dout = nullptr;
+  CK(cudaMalloc(&drows, sizeof(int32_t) * std::max(nrows, 1)));
+  CK(cudaMalloc(&dout, sizeof(double) * std::max<size_t>(1, static_cast<size_t>(nrows) * n)));
+  CK(cudaMemcpyAsync(drows, rows, sizeof(int32_t) * nrows, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_read_rows(ctx->d, drows, nrows, dout, ctx->stream));
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * static_cast<size_t>(nrows) * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(drows);
+  cudaFree(dout);
+  return LSAPGPU_OK;
+}
+
+void lsapgpu_random_perm(int32_t n, uint64_t seed, int32_t* p) {
+  // rng.hpp:37-46 (Fisher-Yates over splitmix64)
+  for (int32_t i = 0; i < n; ++i) p[i] = i;
+  uint64_t state = seed;
+  for (int32_t i = n - 1; i > 0; --i) {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    const int32_t j = static_cast<int32_t>(z % static_cast<uint64_t>(i + 1));
+    std::swap(p[i], p[j]);
+  }
+}
+
+int lsapgpu_objective(lsapgpu_ctx* ctx, const int32_t* sigma, double* value) {
+  if (!ctx || !ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  CK(cudaSetDevice(ctx->device));
+  const int32_t n = ctx->n_matrix;
+  if (!is_perm(sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
+  CK(cudaMemcpyAsync(ctx->d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  return device_objective(ctx, value);
+}
+
+int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  ctx->timing = enabled != 0;
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
+                        double* full_sweep_ms, int64_t* full_sweeps) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (total_ms) *total_ms = ctx->scan_ms;
+  if (launches) *launches = ctx->scan_launches;
+  if (full_sweep_ms) *full_sweep_ms = ctx->full_ms;
+  if (full_sweeps) *full_sweeps = ctx->full_launches;
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_evaluate_all(lsapgpu_ctx* ctx, const int32_t* sigma, double eps, double* agent_delta,
+                         int32_t* agent_partner, double* job_delta, int32_t* job_partner) {
+  if (!ctx || !ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  CK(cudaSetDevice(ctx->device));
+  if (!(eps >= 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "improvement_epsilon must be >= 0");
+  const int32_t n = ctx->n_matrix;
+  if (!is_perm(sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
+  DevState& d = ctx->d;
+  d.eps = eps;
+  CK(cudaMemcpyAsync(d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_init_assignment(d, ctx->stream));
+  begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+  CK(cudaGetLastError());
+  int rc = run_scan(ctx, 1);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(agent_delta, d.agent_delta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(agent_partner, d.agent_partner, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(job_delta, d.job_delta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(job_partner, d.job_partner, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_delta,
+                            const int32_t* agent_partner, const double* job_delta,
+                            const int32_t* job_partner, const int32_t* sigma,
+                            uint8_t* agent_accepted, uint8_t* job_accepted, uint8_t* reserved_mask,
+                            uint8_t* conflicted_mask, int32_t* conflicted_jobs,
+                            int32_t* n_conflicted_jobs) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "delta tables do not match assignment size");
+  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  for (int32_t k = 0; k < n; ++k)
+    if (agent_partner[k] >= n || job_partner[k] >= n || agent_partner[k] < -1 || job_partner[k] < -1)
+      return fail(ctx, LSAPGPU_ERR_INVALID, "record partner out of range");
+  if (!is_perm(sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
+  if (ctx->n_vec != n) ctx->n_matrix = 0;
+  int rc = ensure_vectors(ctx, n);
+  if (rc) return rc;
+  DevState d = ctx->d;
+  if (!ctx->n_matrix) d.storage = kI32;  // the commit kernel template needs some storage type
+  CK(cudaMemcpyAsync(d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.agent_delta, agent_delta, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.job_delta, job_delta, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.job_partner, job_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+  CK(cudaGetLastError());
+  CK(launch_edges_from_tables(d, ctx->stream));
+  CK(launch_commit(d, plan_commit(d), kCommitCheckOnly, 0, 0, ctx->stream));
+  rc = pull_ctrl(ctx);
+  if (rc) return rc;
+  const int32_t m = ctx->ctrl_host->edge_count[ctx->ctrl_host->parity];
+  std::vector<int32_t> slots(m), eu(m), ev(m);
+  std::vector<uint8_t> est(m);
+  if (m) {
+    const int P = ctx->ctrl_host->parity;
+    CK(cudaMemcpyAsync(slots.data(), d.edges[P], sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(eu.data(), d.eu, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ev.data(), d.ev, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(est.data(), d.estate, m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  std::memset(agent_accepted, 0, n);
+  std::memset(job_accepted, 0, n);
+  std::memset(reserved_mask, 0, n);
+  std::memset(conflicted_mask, 0, n);
+  std::vector<int32_t> cj;
+  for (int32_t e = 0; e < m; ++e) {
+    const int32_t s = slots[e];
+    if (est[e] == kEdgeAccepted) {
+      (s < n ? agent_accepted[s] : job_accepted[s - n]) = 1;
+      reserved_mask[eu[e]] = 1;
+      reserved_mask[ev[e]] = 1;
+    } else if (est[e] == kEdgeRejected) {
+      conflicted_mask[eu[e]] = 1;  // the proposer (the job's holder on the job side)
+      if (s >= n) cj.push_back(s - n);
+    }
+  }
+  std::sort(cj.begin(), cj.end());
+  for (size_t k = 0; k < cj.size(); ++k) conflicted_jobs[k] = cj[k];
+  *n_conflicted_jobs = static_cast<int32_t>(cj.size());
+  // restore the edge lists for the next user
+  ctx->ctrl_host->edge_count[0] = ctx->ctrl_host->edge_count[1] = 0;
+  return push_ctrl(ctx);
+}
+
+int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* tau, double* value,
+                                    const double* agent_delta, const int32_t* agent_partner,
+                                    const uint8_t* agent_active, const double* job_delta,
+                                    const int32_t* job_partner, const uint8_t* job_active,
+                                    const uint8_t* agent_accepted, const uint8_t* job_accepted,
+                                    double eps, int32_t* applied_agent, int32_t* applied_new_job,
+                                    int32_t* applied_old_job, int32_t* applied_displaced,
+                                    double* applied_delta, int32_t* n_applied) {
+  if (!ctx || !ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  CK(cudaSetDevice(ctx->device));
+  if (!(eps >= 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "improvement_epsilon must be >= 0");
+  const int32_t n = ctx->n_matrix;
+  if (!is_perm(sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "assignment does not match instance");
+  for (int32_t k = 0; k < n; ++k)
+    if (agent_partner[k] >= n || job_partner[k] >= n) return fail(ctx, LSAPGPU_ERR_INVALID, "record partner out of range");
+  DevState& d = ctx->d;
+  d.eps = eps;
+  // active flag folded into the delta, exactly as the select guard reads it
+  std::vector<double> ad(n), jd(n);
+  for (int32_t k = 0; k < n; ++k) {
+    ad[k] = agent_active[k] ? agent_delta[k] : 0.0;
+    jd[k] = job_active[k] ? job_delta[k] : 0.0;
+  }
+  uint8_t* masks = nullptr;
+  CK(cudaMalloc(&masks, 2 * static_cast<size_t>(n)));
+  CK(cudaMemcpyAsync(masks, agent_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(masks + n, job_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.tau, tau, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.agent_delta, ad.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.job_delta, jd.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d.job_partner, job_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+  CK(cudaGetLastError());
+  CK(launch_edges_from_tables(d, ctx->stream));
+  CK(launch_accepted_from_masks(d, masks, masks + n, ctx->stream));
+  int rc = pull_ctrl(ctx);
+  cudaFree(masks);
+  if (rc) return rc;
+  Ctrl& C = *ctx->ctrl_host;
+  const int64_t cnt = C.log_count;
+  std::vector<LogEntry> log(static_cast<size_t>(cnt));
+  if (cnt) {
+    CK(cudaMemcpyAsync(log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  const int err = C.error;
+  C.error = 0;
+  C.log_count = 0;
+  C.edge_count[0] = C.edge_count[1] = 0;
+  rc = push_ctrl(ctx);
+  if (rc) return rc;
+  if (err) return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
+  std::sort(log.begin(), log.end(), [](const LogEntry& a, const LogEntry& b) { return a.slot < b.slot; });
+  // applied list in the reference's commit order, recovered from the frozen input
+  std::vector<int32_t> s0(sigma, sigma + n), t0(tau, tau + n);
+  double v = *value;
+  int32_t k = 0;
+  for (const auto& L : log) {
+    int32_t agent, j_new;
+    if (L.slot < n) {
+      agent = L.slot;
+      j_new = agent_partner[L.slot];
+    } else {
+      agent = job_partner[L.slot - n];
+      j_new = L.slot - n;
+    }
+    const int32_t j_old = t0[agent], disp = s0[j_new];
+    applied_agent[k] = agent;
+    applied_new_job[k] = j_new;
+    applied_old_job[k] = j_old;
+    applied_displaced[k] = disp;
+    applied_delta[k] = L.delta;
+    sigma[j_new] = agent;
+    sigma[j_old] = disp;
+    tau[agent] = j_new;
+    tau[disp] = j_old;
+    v += L.delta;
+    ++k;
+  }
+  *value = v;
+  *n_applied = k;
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma_out,
+                  int32_t* tau_out, lsapgpu_stats* stats, int64_t* trace_switch, double* trace_value,
+                  int64_t trace_cap, int64_t* trace_len) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (!ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  if (!params || !sigma_out) return fail(ctx, LSAPGPU_ERR_INVALID, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  const auto t_start = std::chrono::steady_clock::now();
+  const lsapgpu_params& P = *params;
+  if (!(P.eps >= 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "improvement_epsilon must be >= 0");
+  if (P.reeval != 0 && P.reeval != 1) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown reeval policy");
+  const int32_t n = ctx->n_matrix;
+  DevState& d = ctx->d;
+
+  std::vector<int32_t> sigma0(n);
+  if (P.init_sigma) {
+    if (!is_perm(P.init_sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
+    std::copy(P.init_sigma, P.init_sigma + n, sigma0.begin());
+  } else {
+    lsapgpu_random_perm(n, P.seed, sigma0.data());
+  }
+  CK(cudaMemcpyAsync(d.sigma, sigma0.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_init_assignment(d, ctx->stream));
+  double value = 0.0;
+  int rc = device_objective(ctx, &value);
+  if (rc) return rc;
+
+  TraceSink trace{trace_switch, trace_value, trace_cap};
+  trace.push(0, value);
+  lsapgpu_stats S;
+  std::memset(&S, 0, sizeof(S));
+  S.storage = d.storage;
+
+  auto elapsed_ns = [&]() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_start)
+        .count();
+  };
+  bool expired = P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns;
+
+  d.eps = P.eps;
+  d.policy = P.reeval;
+  if (!expired) {
+    set_deadline_kernel<<<1, 1, 0, ctx->stream>>>(
+        ctx->ctrl_dev, P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns()));
+    CK(cudaGetLastError());
+    if (P.use_graph && (!ctx->exec || ctx->graph_eps != d.eps || ctx->graph_policy != d.policy)) {
+      rc = build_graph(ctx);
+      if (rc) return rc;
+    }
+  }
+  ctx->scan_ms = ctx->full_ms = 0.0;
+  ctx->scan_launches = ctx->full_launches = 0;
+
+  rc = pull_ctrl(ctx);
+  if (rc) return rc;
+  const Ctrl base = *ctx->ctrl_host;  // counters are cumulative per context
+  std::vector<LogEntry> log;
+  int64_t switches = 0;
+  int64_t launches = 0;
+
+  while (!expired) {
+    ++S.outer_iterations;
+    const double f_start = value;
+    begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+    CK(cudaGetLastError());
+    rc = run_scan(ctx, 1);
+    if (rc) return rc;
+    ++launches;
+    S.pair_items += n;
+    S.agent_scans += n;
+    S.job_scans += n;
+    for (;;) {  // inner loop; repeats only to drain a full delta log
+      if (P.use_graph) {
+        CK(cudaGraphLaunch(ctx->exec, ctx->stream));
+        rc = pull_ctrl(ctx);
+        if (rc) return rc;
+      } else {
+        for (;;) {
+          CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
+          rc = run_scan(ctx, 0);
+          if (rc) return rc;
+          ++launches;
+          rc = pull_ctrl(ctx);
+          if (rc) return rc;
+          const Ctrl& C = *ctx->ctrl_host;
+          if (C.inner_done || C.expired || C.drain || C.error) break;
+        }
+      }
+      Ctrl& C = *ctx->ctrl_host;
+      if (C.error) {
+        C.error = 0;
+        push_ctrl(ctx);
+        return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
+      }
+      const int64_t cnt = C.log_count;
+      log.resize(static_cast<size_t>(cnt));
+      if (cnt) {
+        CK(cudaMemcpyAsync(log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+      }
+      // batch order: iteration, then ascending slot (agents then jobs)
+      std::sort(log.begin(), log.end(), [](const LogEntry& a, const LogEntry& b) {
+        return a.iter != b.iter ? a.iter < b.iter : a.slot < b.slot;
+      });
+      for (const auto& L : log) {
+        value += L.delta;
+        ++switches;
+        trace.push(switches, value);
+      }
+      const bool drained = C.drain;
+      if (C.expired) expired = true;
+      begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);  // log_count = 0, drain = 0
+      CK(cudaGetLastError());
+      if (!drained || expired) break;
+    }
+    if (expired) break;
+    if (P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns) {
+      expired = true;
+      break;
+    }
+    if (trace.len >= kTraceCap) trace.push(switches, value, true);
+    if (value == f_start) break;
+  }
+
+  rc = pull_ctrl(ctx);
+  if (rc) return rc;
+  const Ctrl& C = *ctx->ctrl_host;
+  S.inner_iterations = C.inner_iterations - base.inner_iterations;
+  S.pair_items += C.pair_items - base.pair_items;
+  S.agent_scans += C.agent_scans - base.agent_scans;
+  S.job_scans += C.job_scans - base.job_scans;
+  S.lfmm_rounds = C.lfmm_rounds - base.lfmm_rounds;
+  S.switches_applied = switches;
+  S.scan_launches = P.use_graph ? S.outer_iterations + S.inner_iterations : launches;
+  S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
+  S.terminated_by = expired ? 1 : 0;
+
+  CK(cudaMemcpyAsync(sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tau_out) CK(cudaMemcpyAsync(tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  double final_value = 0.0;
+  rc = device_objective(ctx, &final_value);  // snapshot_assignment, solver_state.hpp:141-148
+  if (rc) return rc;
+  S.value = final_value;
+  S.elapsed_ms = static_cast<double>(elapsed_ns()) / 1e6;
+  if (stats) *stats = S;
+  if (trace_len) *trace_len = trace.len;
+  return LSAPGPU_OK;
+}
+
+}  // extern "C"

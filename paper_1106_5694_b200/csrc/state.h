@@ -1,0 +1,114 @@
+// state.h -- device-resident solver state shared by the host orchestration
+// (lsapgpu.cu) and the kernels (layout.cu, scan.cu, commit.cu).
+//
+// It is the B200 layout of the reference's detail::SolverState
+// (proj/src/solver_state.hpp:33-149): the same vectors (sigma, tau, the
+// per-agent current benefit, SoA delta tables), plus the work list, the
+// ping-pong active-edge lists that replace argmax + check_conflicts' linear
+// walks, and the delta log that replaces the in-loop value/trace update.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace lsapgpu {
+
+struct DevState {
+  int32_t n = 0;
+  int64_t ld = 0;  // row pitch in elements (multiple of 64)
+  int storage = kF64;
+  const void* A = nullptr;   // row-major, n x ld
+  const void* AT = nullptr;  // transposed, n x ld
+  int32_t* sigma = nullptr;  // job -> agent (padded to ld)
+  int32_t* tau = nullptr;    // agent -> job (padded to ld)
+  void* acur = nullptr;      // A[i][tau[i]] (storage type, padded to ld)
+
+  double* agent_delta = nullptr;
+  int32_t* agent_partner = nullptr;
+  double* job_delta = nullptr;
+  int32_t* job_partner = nullptr;
+
+  int32_t* edges[2] = {nullptr, nullptr};  // active record slots, capacity 2n each
+  int32_t* eu = nullptr;                   // LFMM scratch: endpoint u, capacity 2n
+  int32_t* ev = nullptr;                   // endpoint v
+  int32_t* eprop = nullptr;                // proposer agent (frozen sigma)
+  uint8_t* estate = nullptr;               // edge state
+  int32_t* c_jnew = nullptr;               // committed exchange: new job
+  double* c_delta = nullptr;               // committed exchange: recomputed delta
+  uint32_t* keys = nullptr;                // vertex keys when they do not fit in smem
+  int32_t* touched_stamp = nullptr;        // agent touched in iteration k
+  int32_t* conf_stamp = nullptr;           // agent queued as conflicted in iteration k
+  int32_t* rej_stamp = nullptr;            // record slot rejected in iteration k (2n)
+  uint32_t* items = nullptr;               // work list (capacity n)
+  LogEntry* log = nullptr;                 // committed exchanges, ordered by (iter, slot) on the host
+  int64_t log_cap = 0;
+
+  // split-item partial results (segmented scans)
+  double* part_ad = nullptr;
+  int32_t* part_at = nullptr;
+  double* part_jd = nullptr;
+  int32_t* part_ji = nullptr;
+  int32_t* part_arrive = nullptr;  // per item-group arrival counters (zeroed)
+  int64_t part_cap = 0;            // capacity in (item, segment) slots
+
+  Ctrl* ctrl = nullptr;
+  double eps = 0.0;
+  int policy = 0;  // 0 touched_and_conflicted, 1 touched_only
+};
+
+// ---- launchers (implemented in the .cu files) -------------------------------
+
+// layout.cu
+struct LayoutSource {
+  int kind = 0;  // 0 memory, 1 uniform int, 2 unit f32, 3 unit scaled, 4 p2p, 5 geom
+  const void* src = nullptr;  // memory source (row-major n x n)
+  int src_dtype = 0;          // 0 f64, 1 f32, 2 i32, 3 i16
+  uint64_t seed = 0;
+  double param = 0.0;
+  const double* aux = nullptr;  // generator side tables (p2p: up,x,y; geom: xs,ys)
+};
+// flags bit0: non-finite present, bit1: not int16-exact, bit2: not int32 (<2^29) exact,
+// bit3: not fp32-exact.
+cudaError_t launch_classify(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
+                            uint32_t* flags, cudaStream_t st);
+cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
+                                int storage, void* A, void* AT, int64_t ld, cudaStream_t st);
+cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaStream_t st);
+cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st);  // tau, acur from sigma
+cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st);
+cudaError_t launch_read_rows(const DevState& d, const int32_t* rows, int32_t nrows, double* out,
+                             cudaStream_t st);
+
+// scan.cu
+struct ScanPlan {
+  int m = 1;            // items batched per CTA (share tau/acur streams)
+  int passes = 1;       // row chunks per item (rows larger than smem)
+  int64_t chunk = 0;    // elements per staged chunk
+  int bufs = 2;         // smem stage buffers
+  int ctas = 0;         // persistent grid size
+  int threads = 256;
+  size_t smem = 0;      // dynamic smem per CTA
+  int max_segments = 1;
+};
+ScanPlan plan_scan(const DevState& d, int num_sms);
+// full sweep (identity work list, count n) when full != 0, else the device work list
+cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+
+// commit.cu
+enum CommitMode : int { kCommitSolve = 0, kCommitCheckOnly = 1, kCommitApplyOnly = 2 };
+struct CommitPlan {
+  int threads = 1024;
+  size_t smem = 0;
+  bool keys_in_smem = true;
+};
+CommitPlan plan_commit(const DevState& d);
+cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
+                          cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st);
+// step-API helpers
+cudaError_t launch_edges_from_tables(const DevState& d, cudaStream_t st);
+cudaError_t launch_accepted_from_masks(const DevState& d, const uint8_t* agent_acc,
+                                       const uint8_t* job_acc, cudaStream_t st);
+
+}  // namespace lsapgpu

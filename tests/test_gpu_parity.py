@@ -1,0 +1,400 @@
+"""GPU parity suite: the CUDA path (through the C-ABI) against the oracle.
+
+Mirrors the reference's own tests (paths relative to /root/reference/proj):
+tests/test_parallel.cpp (evaluate_all bit-identity, conflict-check hand cases,
+apply semantics, dgs_parallel fidelity / fixed point / trace / deadline) and
+tests/acceptance.cpp:133-159 (fidelity at n in {64, 256, 1024}).  Bit-exact:
+sigma, tau, value, outer iterations, switch count and the full objective
+trace must equal the oracle's.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _g():
+    import paper_1106_5694_b200 as g
+    return g
+
+
+def assert_same_solve(rep, ref):
+    assert np.array_equal(rep.assignment.sigma, ref.sigma)
+    assert np.array_equal(rep.assignment.tau, ref.tau)
+    assert rep.assignment.value == ref.value
+    assert rep.outer_iterations == ref.outer_iterations
+    assert rep.switches_applied == ref.switches_applied
+    assert rep.terminated_by == ref.terminated_by
+    assert rep.objective_trace == ref.trace
+
+
+def tables_equal(t, ad, ap, jd, jp):
+    return (np.array_equal(t.agent_partner, ap) and np.array_equal(t.job_partner, jp)
+            and np.array_equal(t.agent_delta.view(np.uint64), ad.view(np.uint64))
+            and np.array_equal(t.job_delta.view(np.uint64), jd.view(np.uint64)))
+
+
+# ---------------------------------------------------------------------------
+# evaluate_all_parallel  (test_parallel.cpp:47-76)
+# ---------------------------------------------------------------------------
+def test_evaluate_all_bit_identical_small_fp64(oracle, gpu_ctx):
+    for seed in range(10):
+        n = 3 + (seed * 7 % 62)
+        a = oracle.generate("unit", n, 800 + seed, 10.0)
+        sigma = oracle.random_perm(n, seed)
+        gpu_ctx.set_matrix(a)
+        assert gpu_ctx.storage == "fp64"
+        t = gpu_ctx.evaluate_all(sigma)
+        assert tables_equal(t, *oracle.evaluate_all(a, sigma)), f"seed {seed} n {n}"
+
+
+@pytest.mark.parametrize("kind,n,storage", [
+    ("int", 300, "int16"), ("p2p", 777, "int16"), ("f32", 513, "fp32"), ("geom", 256, "fp64"),
+    ("int", 1, "int16"), ("int", 2, "int16"), ("geom", 65, "fp64")])
+def test_evaluate_all_kinds(oracle, gpu_ctx, kind, n, storage):
+    a = oracle.generate(kind, n, 41)
+    sigma = oracle.random_perm(n, 3)
+    gpu_ctx.set_matrix(a)
+    assert gpu_ctx.storage == storage
+    t = gpu_ctx.evaluate_all(sigma)
+    assert tables_equal(t, *oracle.evaluate_all(a, sigma))
+
+
+def test_evaluate_all_int32_storage_and_eps(oracle, gpu_ctx):
+    n = 200
+    a = oracle.generate("int", n, 5, 1 << 20)  # needs int32
+    gpu_ctx.set_matrix(a)
+    assert gpu_ctx.storage == "int32"
+    sigma = oracle.random_perm(n, 9)
+    for eps in (0.0, 3.0, 1e5):
+        t = gpu_ctx.evaluate_all(sigma, eps)
+        assert tables_equal(t, *oracle.evaluate_all(a, sigma, eps))
+
+
+def test_evaluate_all_ties(oracle, gpu_ctx):
+    """Forced value ties: the smallest candidate index must win on both sides."""
+    n = 150
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 3, size=(n, n)).astype(np.float64)
+    sigma = oracle.random_perm(n, 1)
+    gpu_ctx.set_matrix(a)
+    t = gpu_ctx.evaluate_all(sigma)
+    assert tables_equal(t, *oracle.evaluate_all(a, sigma))
+
+
+def test_matrix_dtypes_and_device_upload(oracle, gpu_ctx):
+    import torch
+    n = 100
+    a = oracle.generate("int", n, 7)
+    sigma = oracle.random_perm(n, 2)
+    expect = oracle.evaluate_all(a, sigma)
+    for arr in (a, a.astype(np.float32), a.astype(np.int32), a.astype(np.int16),
+                torch.from_numpy(a).cuda(), torch.from_numpy(a.astype(np.float32)).cuda()):
+        gpu_ctx.set_matrix(arr)
+        assert gpu_ctx.storage == "int16"
+        assert tables_equal(gpu_ctx.evaluate_all(sigma), *expect)
+
+
+def test_generators_match_oracle(oracle, gpu_ctx):
+    for kind, n, seed, param in [("int", 70, 3, 1000), ("f32", 70, 4, None), ("unit", 70, 5, 10.0),
+                                 ("p2p", 70, 6, None), ("geom", 70, 7, 100.0)]:
+        gpu_ctx.generate(kind, n, seed, param)
+        a = oracle.generate(kind, n, seed, param)
+        got = gpu_ctx.read_rows(np.arange(n))
+        assert np.array_equal(got.view(np.uint64), a.view(np.uint64)), kind
+
+
+@pytest.mark.parametrize("env", [
+    {"LSAPGPU_SCAN_M": "1"}, {"LSAPGPU_SCAN_M": "2"}, {"LSAPGPU_SCAN_M": "4"},
+    {"LSAPGPU_SCAN_BUDGET": "3072"},                                   # 4 passes, single buffer
+    {"LSAPGPU_SCAN_BUDGET": "9000", "LSAPGPU_SCAN_M": "1"},            # single-buffered rows
+    {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # split items over CTAs
+])
+def test_scan_plan_variants_subprocess(env):
+    """Every scan-plan code path (batching, chunked passes, segments) is bit-exact.
+
+    The plan is read from the environment when the matrix is set, so each
+    variant runs in a fresh process."""
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_1106_5694_b200 as g\n"
+        "from oracle.oracle import Oracle\n"
+        "o = Oracle(); ctx = g.Context(0)\n"
+        "for kind, n in [('f32', 1000), ('int', 700), ('geom', 300)]:\n"
+        "    a = o.generate(kind, n, 11); s = o.random_perm(n, 4)\n"
+        "    ctx.set_matrix(a); t = ctx.evaluate_all(s)\n"
+        "    ad, ap, jd, jp = o.evaluate_all(a, s)\n"
+        "    assert np.array_equal(t.agent_partner, ap) and np.array_equal(t.job_partner, jp), kind\n"
+        "    assert np.array_equal(t.agent_delta, ad) and np.array_equal(t.job_delta, jd), kind\n"
+        "    r = ctx.solve(g.ParallelConfig(seed=2)); q = o.dgs_parallel(a, seed=2)\n"
+        "    assert np.array_equal(r.assignment.sigma, q.sigma) and r.objective_trace == q.trace, kind\n"
+        "print('ok')\n" % ROOT)
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------------------
+# check_conflicts  (test_parallel.cpp:78-128) + randomized vs the oracle
+# ---------------------------------------------------------------------------
+def _tables(n):
+    return _g().DeltaTables.sized(n)
+
+
+def test_check_conflicts_hand_cases(gpu_ctx):
+    g = _g()
+    ident = np.arange(4, dtype=np.int32)
+    t = _tables(4)
+    s = gpu_ctx.check_conflicts(t, ident)
+    assert s.reserved == [] and s.conflicted == [] and s.conflicted_jobs == []
+
+    t = _tables(4)
+    t.set_agent(0, g.ExchangeRecord(2, 1.0, True))
+    t.set_agent(1, g.ExchangeRecord(3, 2.0, True))
+    s = gpu_ctx.check_conflicts(t, ident)
+    assert s.reserved == [0, 1, 2, 3] and s.conflicted == []
+    assert s.agent_accepted[0] and s.agent_accepted[1]
+
+    t = _tables(4)
+    t.set_agent(0, g.ExchangeRecord(2, 1.0, True))
+    t.set_agent(1, g.ExchangeRecord(2, 2.0, True))
+    s = gpu_ctx.check_conflicts(t, ident)
+    assert s.reserved == [0, 2] and s.conflicted == [1]
+    assert s.agent_accepted[0] and not s.agent_accepted[1]
+
+    t = _tables(4)
+    t.set_job(0, g.ExchangeRecord(1, 1.0, True))
+    t.set_job(1, g.ExchangeRecord(0, 1.0, True))
+    t.set_job(2, g.ExchangeRecord(3, 1.0, True))
+    s = gpu_ctx.check_conflicts(t, ident)
+    assert s.reserved == [0, 1, 2, 3] and s.conflicted == [1] and s.conflicted_jobs == [1]
+    assert s.job_accepted[0] and not s.job_accepted[1] and s.job_accepted[2]
+
+
+@pytest.mark.parametrize("n,density,seed", [(50, 0.9, 1), (400, 0.5, 2), (3000, 0.95, 3), (2000, 0.05, 4)])
+def test_check_conflicts_random_vs_oracle(oracle, gpu_ctx, n, density, seed):
+    """Random proposal graphs (dense conflicts): LFMM rounds == sequential walk."""
+    rng = np.random.default_rng(seed)
+    sigma = rng.permutation(n).astype(np.int32)
+    t = _tables(n)
+    for side in ("agent", "job"):
+        act = rng.random(n) < density
+        part = rng.integers(0, n, n).astype(np.int32)
+        own = np.arange(n) if side == "agent" else sigma  # partner must differ from self
+        if side == "agent":
+            tau = np.empty(n, np.int32)
+            tau[sigma] = np.arange(n)
+            bad = part == tau
+        else:
+            bad = part == sigma
+        part[bad] = (part[bad] + 1) % n
+        del own
+        delta = np.where(act, rng.integers(1, 5, n).astype(np.float64), 0.0)
+        part = np.where(act, part, -1).astype(np.int32)
+        setattr(t, f"{side}_delta", delta)
+        setattr(t, f"{side}_partner", part)
+        setattr(t, f"{side}_active", act.astype(np.uint8))
+    s = gpu_ctx.check_conflicts(t, sigma)
+    o = oracle.check_conflicts(t.agent_delta, t.agent_partner, t.job_delta, t.job_partner, sigma)
+    assert np.array_equal(s.agent_accepted, o["agent_accepted"])
+    assert np.array_equal(s.job_accepted, o["job_accepted"])
+    assert s.reserved == np.flatnonzero(o["reserved"]).tolist()
+    assert s.conflicted == np.flatnonzero(o["conflicted"]).tolist()
+    assert s.conflicted_jobs == o["conflicted_jobs"].tolist()
+
+
+# ---------------------------------------------------------------------------
+# apply_parallel_switches  (test_parallel.cpp:130-194)
+# ---------------------------------------------------------------------------
+def test_apply_nothing_survives_when_all_conflict(oracle):
+    g = _g()
+    inst = g.Instance.from_matrix(oracle.generate("unit", 4, 9, 10.0))
+    asg = g.make_assignment(inst, [0, 1, 2, 3])
+    t = _tables(4)
+    t.set_agent(0, g.ExchangeRecord(2, 1.0, True))
+    t.set_agent(1, g.ExchangeRecord(2, 2.0, True))
+    sets = g.check_conflicts(t, asg)
+    sets.agent_accepted[0] = 0
+    out, applied = g.apply_parallel_switches(inst, asg, t, sets)
+    assert applied == [] and np.array_equal(out.sigma, asg.sigma) and out.value == asg.value
+
+
+def test_apply_singleton_and_additive(oracle):
+    g = _g()
+    inst = g.Instance.from_matrix(oracle.generate("unit", 5, 10, 10.0))
+    asg = g.make_assignment(inst, oracle.random_perm(5, 2))
+    t = _tables(5)
+    g.evaluate_all_parallel(inst, asg, t)
+    chosen = next(i for i in range(5) if t.agent_active[i])
+    for i in range(5):
+        if i != chosen:
+            t.set_agent(i, g.ExchangeRecord())
+    t.job_partner[:] = -1
+    t.job_delta[:] = 0
+    t.job_active[:] = 0
+    sets = g.check_conflicts(t, asg)
+    out, applied = g.apply_parallel_switches(inst, asg, t, sets)
+    assert len(applied) == 1
+    j = int(t.agent_partner[chosen])
+    d = g.agent_exchange_delta(inst, asg, chosen, j)
+    assert applied[0].delta == d and out.value == asg.value + d
+
+    m = np.ones((8, 8))
+    m[0, 1] = m[1, 0] = 9
+    m[4, 5] = m[5, 4] = 7
+    inst = g.Instance.from_matrix(m)
+    asg = g.make_assignment(inst, np.arange(8))
+    t = _tables(8)
+    g.evaluate_all_parallel(inst, asg, t)
+    sets = g.check_conflicts(t, asg)
+    out, applied = g.apply_parallel_switches(inst, asg, t, sets)
+    assert len(applied) == 2
+    assert out.value == asg.value + applied[0].delta + applied[1].delta
+
+
+def test_apply_random_vs_oracle(oracle, gpu_ctx):
+    n = 600
+    a = oracle.generate("f32", n, 77)
+    sigma = oracle.random_perm(n, 5)
+    tau = np.empty(n, np.int32)
+    tau[sigma] = np.arange(n)
+    value = oracle.objective(a, sigma)
+    ad, ap, jd, jp = oracle.evaluate_all(a, sigma)
+    cc = oracle.check_conflicts(ad, ap, jd, jp, sigma)
+    aa, ja = (ap >= 0).astype(np.uint8), (jp >= 0).astype(np.uint8)
+    s1, t1, v1, app1 = oracle.apply_parallel_switches(a, sigma, tau, value, (ad, ap, aa, jd, jp, ja),
+                                                      cc["agent_accepted"], cc["job_accepted"])
+    g = _g()
+    gpu_ctx.set_matrix(a)
+    t = g.DeltaTables(n)
+    t.agent_delta, t.agent_partner, t.agent_active = ad, ap, aa
+    t.job_delta, t.job_partner, t.job_active = jd, jp, ja
+    sets = g.ConflictSets([], [], cc["agent_accepted"], cc["job_accepted"], [])
+    out, applied = gpu_ctx.apply_parallel_switches(g.Assignment(sigma, tau, value), t, sets)
+    assert np.array_equal(out.sigma, s1) and np.array_equal(out.tau, t1) and out.value == v1
+    assert [(x.agent, x.new_job, x.old_job, x.displaced, x.delta) for x in applied] == app1
+
+
+def test_apply_overlap_raises_internal(oracle, gpu_ctx):
+    g = _g()
+    n = 6
+    a = np.ones((n, n))
+    a[0, 2] = a[2, 0] = 10
+    a[1, 2] = a[2, 1] = 12
+    gpu_ctx.set_matrix(a)
+    ident = np.arange(n, dtype=np.int32)
+    t = _tables(n)
+    t.set_agent(0, g.ExchangeRecord(2, 18.0, True))
+    t.set_agent(1, g.ExchangeRecord(2, 22.0, True))
+    sets = g.ConflictSets([], [], np.array([1, 1, 0, 0, 0, 0], np.uint8), np.zeros(n, np.uint8), [])
+    with pytest.raises(g.InternalError, match="overlapping exchanges"):
+        gpu_ctx.apply_parallel_switches(g.Assignment(ident, ident.copy(), 6.0), t, sets)
+
+
+# ---------------------------------------------------------------------------
+# dgs_parallel  (test_parallel.cpp:196-283, acceptance.cpp:133-159)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("kind,n,iseed,seed", [
+    ("int", 1000, 0, 0),            # C1
+    ("geom", 64, 47 + 64, 12), ("geom", 128, 47 + 128, 12),
+    ("unit", 50, 800, 3), ("unit", 7, 9501, 2), ("int", 2, 0, 0), ("int", 1, 0, 0),
+    ("f32", 2000, 0, 0), ("p2p", 2000, 0, 0), ("p2p", 3001, 5, 9),
+])
+def test_dgs_parallel_bit_exact(oracle, gpu_ctx, kind, n, iseed, seed):
+    a = oracle.generate(kind, n, iseed)
+    gpu_ctx.set_matrix(a)
+    rep = gpu_ctx.solve(_g().ParallelConfig(seed=seed))
+    assert_same_solve(rep, oracle.dgs_parallel(a, seed=seed))
+
+
+def test_dgs_parallel_acceptance_fidelity(oracle, gpu_ctx):
+    """acceptance.cpp:133-159 instances (GEOM, derive_instance_seed(7, n, 0), seed 5)."""
+    for n in (64, 256, 1024):
+        a = oracle.generate("geom", n, oracle.derive_instance_seed(7, n, 0))
+        gpu_ctx.set_matrix(a)
+        rep = gpu_ctx.solve(_g().ParallelConfig(seed=5))
+        assert_same_solve(rep, oracle.dgs_parallel(a, seed=5))
+
+
+def test_dgs_parallel_c2_int5000(oracle, gpu_ctx):
+    a = oracle.generate("int", 5000, 0)
+    gpu_ctx.set_matrix(a)
+    rep = gpu_ctx.solve(_g().ParallelConfig(seed=0))
+    assert rep.assignment.value == 4972560.0
+    assert_same_solve(rep, oracle.dgs_parallel(a, seed=0))
+
+
+@pytest.mark.parametrize("policy", ["touched_and_conflicted", "touched_only"])
+@pytest.mark.parametrize("eps", [0.0, 0.05])
+def test_dgs_parallel_policies_and_eps(oracle, gpu_ctx, policy, eps):
+    a = oracle.generate("geom", 300, 59)
+    gpu_ctx.set_matrix(a)
+    rep = gpu_ctx.solve(_g().ParallelConfig(seed=4, reeval=policy, improvement_epsilon=eps))
+    ref = oracle.dgs_parallel(a, seed=4, eps=eps, policy=0 if policy == "touched_and_conflicted" else 1)
+    assert_same_solve(rep, ref)
+
+
+def test_dgs_parallel_fixed_point(oracle, gpu_ctx):
+    """test_parallel.cpp:239-256: no positive 2-exchange remains, both policies."""
+    g = _g()
+    a = oracle.generate("geom", 48, 59)
+    inst = g.Instance.from_matrix(a)
+    for policy in ("touched_and_conflicted", "touched_only"):
+        rep = g.dgs_parallel(inst, g.ParallelConfig(seed=4, reeval=policy))
+        assert rep.terminated_by == "converged"
+        asg = rep.assignment
+        for i in range(inst.n):
+            for j in range(inst.n):
+                if asg.tau[i] != j:
+                    assert g.agent_exchange_delta(inst, asg, i, j) <= 1e-9
+
+
+def test_dgs_parallel_trace_monotone_and_deadline(oracle):
+    g = _g()
+    inst = g.Instance.from_matrix(oracle.generate("geom", 96, 61))
+    rep = g.dgs_parallel(inst, g.ParallelConfig(seed=21))
+    vals = [v for _, v in rep.objective_trace]
+    assert all(b >= a for a, b in zip(vals, vals[1:]))
+    cut = g.dgs_parallel(inst, g.ParallelConfig(seed=21, deadline=0))
+    assert cut.terminated_by == "deadline"
+    assert g.is_permutation(cut.assignment.sigma)
+    assert cut.assignment.value == g.objective(inst, cut.assignment)
+
+
+def test_graph_and_stepped_modes_agree(oracle, gpu_ctx):
+    a = oracle.generate("p2p", 1500, 3)
+    gpu_ctx.set_matrix(a)
+    g = _g()
+    r1 = gpu_ctx.solve(g.ParallelConfig(seed=1, use_graph=True))
+    r2 = gpu_ctx.solve(g.ParallelConfig(seed=1, use_graph=False))
+    assert np.array_equal(r1.assignment.sigma, r2.assignment.sigma)
+    assert r1.objective_trace == r2.objective_trace
+    assert r1.gpu["inner_iterations"] == r2.gpu["inner_iterations"]
+
+
+def test_two_permutation_instance_reaches_optimum():
+    """test_parallel.cpp:196-206."""
+    g = _g()
+    inst = g.Instance(2, [0, 10, 10, 0])
+    for seed in range(6):
+        rep = g.dgs_parallel(inst, g.ParallelConfig(seed=seed, workers=2))
+        assert rep.assignment.value == 20.0 and rep.terminated_by == "converged"
+
+
+def test_errors_match_reference_messages():
+    g = _g()
+    with pytest.raises(g.Error, match="non-finite"):
+        g.dgs_parallel(g.Instance(2, [0.0, float("nan"), 1.0, 2.0]))
+    with pytest.raises(g.Error, match="instance size must be >= 1"):
+        g.dgs_parallel(g.Instance(0, []))
+    with pytest.raises(g.Error, match="improvement_epsilon must be >= 0"):
+        g.dgs_parallel(g.Instance(2, [0, 1, 1, 0]), g.ParallelConfig(improvement_epsilon=-1.0))
+    ctx = g.context(0)
+    with pytest.raises(g.Error, match="non-finite"):
+        ctx.set_matrix(np.array([[1.0, np.inf], [0.0, 1.0]]))
