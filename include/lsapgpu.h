@@ -156,13 +156,21 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
 void lsapgpu_random_perm(int32_t n, uint64_t seed, int32_t* out);
 int lsapgpu_objective(lsapgpu_ctx* ctx, const int32_t* sigma, double* value);
 
+/* Cumulative counters of this context: bytes copied host->device and
+ * device->host by the library, and kernels launched (graph-body kernels
+ * included).  bench.py differences them around its timed region. */
+int lsapgpu_counters(const lsapgpu_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                     int64_t* kernel_launches);
+
 /* Instrumented re-run support for bench.py: time every pair-scan launch of
  * the last host-stepped solve with CUDA events on the launching stream.
- * Returns the summed scan time (ms) and launch count of the last solve that
- * ran with use_graph = 0 and timing enabled. */
+ * Returns the summed pair-scan time (ms) and launch count (and the full-sweep
+ * and commit-kernel shares) of the last solve that ran with use_graph = 0 and
+ * timing enabled. */
 int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled);
 int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
-                        double* full_sweep_ms, int64_t* full_sweeps);
+                        double* full_sweep_ms, int64_t* full_sweeps, double* commit_ms,
+                        int64_t* commit_launches);
 
 #ifdef __cplusplus
 }

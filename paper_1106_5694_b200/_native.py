@@ -25,7 +25,7 @@ EXPORTS = [
     "lsapgpu_last_error", "lsapgpu_stream", "lsapgpu_set_matrix", "lsapgpu_set_matrix_device",
     "lsapgpu_generate", "lsapgpu_n", "lsapgpu_storage", "lsapgpu_read_rows", "lsapgpu_solve",
     "lsapgpu_evaluate_all", "lsapgpu_check_conflicts", "lsapgpu_apply_parallel_switches",
-    "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
+    "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
 ]
 
 
@@ -92,9 +92,10 @@ def _load() -> C.CDLL:
                                                       C.POINTER(i32)]),
         "lsapgpu_random_perm": (None, [i32, u64, vp]),
         "lsapgpu_objective": (C.c_int, [vp, vp, C.POINTER(dbl)]),
+        "lsapgpu_counters": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
         "lsapgpu_set_scan_timing": (C.c_int, [vp, C.c_int]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
-                                          C.POINTER(i64)]),
+                                          C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -83,20 +83,20 @@ __global__ void gen_aux_kernel(LayoutSource s, int32_t n, double* aux) {
 }
 
 __global__ void classify_kernel(Src src, int64_t row0, int64_t rows, uint32_t* flags) {
-  const int64_t total = rows * src.n;
   uint32_t f = 0;
-  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = row0 + k / src.n, j = k % src.n;
-    const double v = src(i, j);
-    if (!isfinite(v)) {
-      f |= 1u | 2u | 4u | 8u;
-      continue;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t i = row0 + r;
+    for (int32_t j = threadIdx.x; j < src.n; j += blockDim.x) {
+      const double v = src(i, j);
+      if (!isfinite(v)) {
+        f |= 1u | 2u | 4u | 8u;
+        continue;
+      }
+      const bool integral = v == trunc(v);
+      if (!(integral && fabs(v) <= 32767.0)) f |= 2u;
+      if (!(integral && fabs(v) < 536870912.0)) f |= 4u;
+      if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
     }
-    const bool integral = v == trunc(v);
-    if (!(integral && fabs(v) <= 32767.0)) f |= 2u;
-    if (!(integral && fabs(v) < 536870912.0)) f |= 4u;
-    if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
   }
   // warp then block OR, one atomic per block
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);

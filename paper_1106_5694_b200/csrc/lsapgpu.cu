@@ -93,8 +93,11 @@ struct lsapgpu_ctx {
   // scan timing (host-stepped mode)
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  double scan_ms = 0.0, full_ms = 0.0;
-  int64_t scan_launches = 0, full_launches = 0;
+  double scan_ms = 0.0, full_ms = 0.0, commit_ms = 0.0;
+  int64_t scan_launches = 0, full_launches = 0, commit_launches = 0;
+
+  // cumulative transfer / launch counters (bench.py's e2e and gpu_launches)
+  int64_t h2d = 0, d2h = 0, launches = 0;
 };
 
 namespace {
@@ -102,6 +105,13 @@ namespace {
 int fail(lsapgpu_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
   return code;
+}
+
+cudaError_t cpy(lsapgpu_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                cudaStream_t st) {
+  if (kind == cudaMemcpyHostToDevice) ctx->h2d += static_cast<int64_t>(bytes);
+  if (kind == cudaMemcpyDeviceToHost) ctx->d2h += static_cast<int64_t>(bytes);
+  return cudaMemcpyAsync(dst, src, bytes, kind, st);
 }
 
 #define CK(expr)                                                                         \
@@ -160,7 +170,7 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.agent_partner, N, true));
   CK(valloc(ctx, &d.job_delta, N, true));
   CK(valloc(ctx, &d.job_partner, N, true));
-  CK(valloc(ctx, &d.edges[0], N2, false));
+  CK(valloc(ctx, &d.edges[0], N2, false));  // int4 proposal entries
   CK(valloc(ctx, &d.edges[1], N2, false));
   CK(valloc(ctx, &d.eu, N2, false));
   CK(valloc(ctx, &d.ev, N2, false));
@@ -186,18 +196,18 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   // Key epochs and iteration stamps restart with fresh (zeroed) vectors.
   std::memset(ctx->ctrl_host, 0, sizeof(Ctrl));
   ctx->ctrl_host->round = 1;
-  CK(cudaMemcpyAsync(ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return LSAPGPU_OK;
 }
 
 int pull_ctrl(lsapgpu_ctx* ctx) {
-  CK(cudaMemcpyAsync(ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return LSAPGPU_OK;
 }
 int push_ctrl(lsapgpu_ctx* ctx) {
-  CK(cudaMemcpyAsync(ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, ctx->ctrl_dev, ctx->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
   return LSAPGPU_OK;
 }
 
@@ -209,8 +219,9 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   drop_graph(ctx);
   CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(uint32_t), ctx->stream));
   CK(launch_classify(src, n, 0, n, ctx->flags_dev, ctx->stream));
+  ++ctx->launches;
   uint32_t flags = 0;
-  CK(cudaMemcpyAsync(&flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, &flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
   int storage = kF64;
@@ -235,6 +246,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   d.AT = static_cast<unsigned char*>(ctx->mat.p) + bytes;
   CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), ld,
                          ctx->stream));
+  ++ctx->launches;
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->scan_plan = plan_scan(d, ctx->num_sms);
   ctx->commit_plan = plan_commit(d);
@@ -256,8 +268,9 @@ int device_objective(lsapgpu_ctx* ctx, double* value) {
   const int32_t n = ctx->d.n;
   double* dv = reinterpret_cast<double*>(ctx->d.c_delta);  // scratch (2n doubles)
   CK(launch_gather_current(ctx->d, dv, ctx->stream));
+  ++ctx->launches;
   std::vector<double> hv(n);
-  CK(cudaMemcpyAsync(hv.data(), dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, hv.data(), dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   double sum = 0.0;
   for (int32_t j = 0; j < n; ++j) sum += hv[j];
@@ -295,6 +308,7 @@ int build_graph(lsapgpu_ctx* ctx) {
 int run_scan(lsapgpu_ctx* ctx, int full) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(launch_scan(ctx->d, ctx->scan_plan, full, ctx->stream));
+  ++ctx->launches;
   if (ctx->timing) {
     CK(cudaEventRecord(ctx->ev1, ctx->stream));
     CK(cudaEventSynchronize(ctx->ev1));
@@ -412,7 +426,7 @@ int lsapgpu_set_matrix(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dt
   const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(n) * src_size(dtype);
   void* stage = nullptr;
   CK(cudaMalloc(&stage, bytes));
-  cudaError_t e = cudaMemcpyAsync(stage, data, bytes, cudaMemcpyHostToDevice, ctx->stream);
+  cudaError_t e = cpy(ctx, stage, data, bytes, cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) {
     cudaFree(stage);
     return fail(ctx, LSAPGPU_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
@@ -457,9 +471,10 @@ int lsapgpu_read_rows(lsapgpu_ctx* ctx, const int32_t* rows, int32_t nrows, doub
   double* dout = nullptr;
   CK(cudaMalloc(&drows, sizeof(int32_t) * std::max(nrows, 1)));
   CK(cudaMalloc(&dout, sizeof(double) * std::max<size_t>(1, static_cast<size_t>(nrows) * n)));
-  CK(cudaMemcpyAsync(drows, rows, sizeof(int32_t) * nrows, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, drows, rows, sizeof(int32_t) * nrows, cudaMemcpyHostToDevice, ctx->stream));
   CK(launch_read_rows(ctx->d, drows, nrows, dout, ctx->stream));
-  CK(cudaMemcpyAsync(out, dout, sizeof(double) * static_cast<size_t>(nrows) * n, cudaMemcpyDeviceToHost,
+  ++ctx->launches;
+  CK(cpy(ctx, out, dout, sizeof(double) * static_cast<size_t>(nrows) * n, cudaMemcpyDeviceToHost,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(drows);
@@ -486,8 +501,17 @@ int lsapgpu_objective(lsapgpu_ctx* ctx, const int32_t* sigma, double* value) {
   CK(cudaSetDevice(ctx->device));
   const int32_t n = ctx->n_matrix;
   if (!is_perm(sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
-  CK(cudaMemcpyAsync(ctx->d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, ctx->d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   return device_objective(ctx, value);
+}
+
+int lsapgpu_counters(const lsapgpu_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                     int64_t* kernel_launches) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (h2d_bytes) *h2d_bytes = ctx->h2d;
+  if (d2h_bytes) *d2h_bytes = ctx->d2h;
+  if (kernel_launches) *kernel_launches = ctx->launches;
+  return LSAPGPU_OK;
 }
 
 int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled) {
@@ -497,8 +521,11 @@ int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled) {
 }
 
 int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
-                        double* full_sweep_ms, int64_t* full_sweeps) {
+                        double* full_sweep_ms, int64_t* full_sweeps, double* commit_ms,
+                        int64_t* commit_launches) {
   if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (commit_ms) *commit_ms = ctx->commit_ms;
+  if (commit_launches) *commit_launches = ctx->commit_launches;
   if (total_ms) *total_ms = ctx->scan_ms;
   if (launches) *launches = ctx->scan_launches;
   if (full_sweep_ms) *full_sweep_ms = ctx->full_ms;
@@ -515,16 +542,18 @@ int lsapgpu_evaluate_all(lsapgpu_ctx* ctx, const int32_t* sigma, double eps, dou
   if (!is_perm(sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
   DevState& d = ctx->d;
   d.eps = eps;
-  CK(cudaMemcpyAsync(d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(launch_init_assignment(d, ctx->stream));
+  ++ctx->launches;
   begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+  ++ctx->launches;
   CK(cudaGetLastError());
   int rc = run_scan(ctx, 1);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(agent_delta, d.agent_delta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(agent_partner, d.agent_partner, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(job_delta, d.job_delta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(job_partner, d.job_partner, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, agent_delta, d.agent_delta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, agent_partner, d.agent_partner, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, job_delta, d.job_delta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, job_partner, d.job_partner, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return LSAPGPU_OK;
 }
@@ -548,26 +577,30 @@ int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_del
   if (rc) return rc;
   DevState d = ctx->d;
   if (!ctx->n_matrix) d.storage = kI32;  // the commit kernel template needs some storage type
-  CK(cudaMemcpyAsync(d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.agent_delta, agent_delta, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.job_delta, job_delta, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.job_partner, job_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.agent_delta, agent_delta, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.job_delta, job_delta, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.job_partner, job_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+  ++ctx->launches;
   CK(cudaGetLastError());
   CK(launch_edges_from_tables(d, ctx->stream));
+  ++ctx->launches;
   CK(launch_commit(d, plan_commit(d), kCommitCheckOnly, 0, 0, ctx->stream));
+  ++ctx->launches;
   rc = pull_ctrl(ctx);
   if (rc) return rc;
   const int32_t m = ctx->ctrl_host->edge_count[ctx->ctrl_host->parity];
-  std::vector<int32_t> slots(m), eu(m), ev(m);
+  std::vector<int4> slots(m);
+  std::vector<int32_t> eu(m), ev(m);
   std::vector<uint8_t> est(m);
   if (m) {
     const int P = ctx->ctrl_host->parity;
-    CK(cudaMemcpyAsync(slots.data(), d.edges[P], sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(eu.data(), d.eu, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(ev.data(), d.ev, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(est.data(), d.estate, m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cpy(ctx, slots.data(), d.edges[P], sizeof(int4) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cpy(ctx, eu.data(), d.eu, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cpy(ctx, ev.data(), d.ev, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cpy(ctx, est.data(), d.estate, m, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
   std::memset(agent_accepted, 0, n);
@@ -576,7 +609,7 @@ int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_del
   std::memset(conflicted_mask, 0, n);
   std::vector<int32_t> cj;
   for (int32_t e = 0; e < m; ++e) {
-    const int32_t s = slots[e];
+    const int32_t s = slots[e].x;
     if (est[e] == kEdgeAccepted) {
       (s < n ? agent_accepted[s] : job_accepted[s - n]) = 1;
       reserved_mask[eu[e]] = 1;
@@ -619,18 +652,21 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
   }
   uint8_t* masks = nullptr;
   CK(cudaMalloc(&masks, 2 * static_cast<size_t>(n)));
-  CK(cudaMemcpyAsync(masks, agent_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(masks + n, job_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.tau, tau, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.agent_delta, ad.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.job_delta, jd.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d.job_partner, job_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, masks, agent_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, masks + n, job_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.tau, tau, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.agent_delta, ad.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.job_delta, jd.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.job_partner, job_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+  ++ctx->launches;
   CK(cudaGetLastError());
   CK(launch_edges_from_tables(d, ctx->stream));
+  ++ctx->launches;
   CK(launch_accepted_from_masks(d, masks, masks + n, ctx->stream));
+  ++ctx->launches;
   int rc = pull_ctrl(ctx);
   cudaFree(masks);
   if (rc) return rc;
@@ -638,7 +674,7 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
   const int64_t cnt = C.log_count;
   std::vector<LogEntry> log(static_cast<size_t>(cnt));
   if (cnt) {
-    CK(cudaMemcpyAsync(log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cpy(ctx, log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
   const int err = C.error;
@@ -701,8 +737,9 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   } else {
     lsapgpu_random_perm(n, P.seed, sigma0.data());
   }
-  CK(cudaMemcpyAsync(d.sigma, sigma0.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cpy(ctx, d.sigma, sigma0.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(launch_init_assignment(d, ctx->stream));
+  ++ctx->launches;
   double value = 0.0;
   int rc = device_objective(ctx, &value);
   if (rc) return rc;
@@ -724,14 +761,15 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   if (!expired) {
     set_deadline_kernel<<<1, 1, 0, ctx->stream>>>(
         ctx->ctrl_dev, P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns()));
+    ++ctx->launches;
     CK(cudaGetLastError());
     if (P.use_graph && (!ctx->exec || ctx->graph_eps != d.eps || ctx->graph_policy != d.policy)) {
       rc = build_graph(ctx);
       if (rc) return rc;
     }
   }
-  ctx->scan_ms = ctx->full_ms = 0.0;
-  ctx->scan_launches = ctx->full_launches = 0;
+  ctx->scan_ms = ctx->full_ms = ctx->commit_ms = 0.0;
+  ctx->scan_launches = ctx->full_launches = ctx->commit_launches = 0;
 
   rc = pull_ctrl(ctx);
   if (rc) return rc;
@@ -739,11 +777,13 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   std::vector<LogEntry> log;
   int64_t switches = 0;
   int64_t launches = 0;
+  int64_t graph_launches = 0;
 
   while (!expired) {
     ++S.outer_iterations;
     const double f_start = value;
     begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
+    ++ctx->launches;
     CK(cudaGetLastError());
     rc = run_scan(ctx, 1);
     if (rc) return rc;
@@ -754,11 +794,22 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
     for (;;) {  // inner loop; repeats only to drain a full delta log
       if (P.use_graph) {
         CK(cudaGraphLaunch(ctx->exec, ctx->stream));
+        ++graph_launches;
         rc = pull_ctrl(ctx);
         if (rc) return rc;
       } else {
         for (;;) {
+          if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
           CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
+          if (ctx->timing) {
+            CK(cudaEventRecord(ctx->ev1, ctx->stream));
+            CK(cudaEventSynchronize(ctx->ev1));
+            float cms = 0.f;
+            CK(cudaEventElapsedTime(&cms, ctx->ev0, ctx->ev1));
+            ctx->commit_ms += cms;
+            ++ctx->commit_launches;
+          }
+          ++ctx->launches;
           rc = run_scan(ctx, 0);
           if (rc) return rc;
           ++launches;
@@ -777,7 +828,7 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
       const int64_t cnt = C.log_count;
       log.resize(static_cast<size_t>(cnt));
       if (cnt) {
-        CK(cudaMemcpyAsync(log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cpy(ctx, log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
       }
       // batch order: iteration, then ascending slot (agents then jobs)
@@ -791,7 +842,8 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
       }
       const bool drained = C.drain;
       if (C.expired) expired = true;
-      begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);  // log_count = 0, drain = 0
+      begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);
+      ++ctx->launches;  // log_count = 0, drain = 0
       CK(cudaGetLastError());
       if (!drained || expired) break;
     }
@@ -813,12 +865,15 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   S.job_scans += C.job_scans - base.job_scans;
   S.lfmm_rounds = C.lfmm_rounds - base.lfmm_rounds;
   S.switches_applied = switches;
-  S.scan_launches = P.use_graph ? S.outer_iterations + S.inner_iterations : launches;
+  S.scan_launches = P.use_graph ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
+  // every body pass of the graph is one commit + one scan launch; the last
+  // pass per graph launch finds no active record and exits early
+  if (P.use_graph) ctx->launches += 2 * (S.inner_iterations + graph_launches);
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 
-  CK(cudaMemcpyAsync(sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (tau_out) CK(cudaMemcpyAsync(tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tau_out) CK(cpy(ctx, tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
   double final_value = 0.0;
   rc = device_objective(ctx, &final_value);  // snapshot_assignment, solver_state.hpp:141-148
   if (rc) return rc;

@@ -30,7 +30,10 @@ struct DevState {
   double* job_delta = nullptr;
   int32_t* job_partner = nullptr;
 
-  int32_t* edges[2] = {nullptr, nullptr};  // active record slots, capacity 2n each
+  // active proposals, capacity 2n each: {slot, a, b, c} with slot = i (agent
+  // record of i: a = i, b = partner job, c = tau[i]) or n + j (job record of j:
+  // a = sigma[j], b = partner agent, c = j), written by the pair scan
+  int4* edges[2] = {nullptr, nullptr};
   int32_t* eu = nullptr;                   // LFMM scratch: endpoint u, capacity 2n
   int32_t* ev = nullptr;                   // endpoint v
   int32_t* eprop = nullptr;                // proposer agent (frozen sigma)
@@ -100,12 +103,18 @@ cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStre
 enum CommitMode : int { kCommitSolve = 0, kCommitCheckOnly = 1, kCommitApplyOnly = 2 };
 struct CommitPlan {
   int threads = 1024;
-  size_t smem = 0;
+  size_t smem = 0;          // single-CTA kernel (apply-only step API)
   bool keys_in_smem = true;
+  int cluster = 8;          // cluster kernel: CTAs per cluster (16 or 8)
+  size_t cluster_smem = 0;  // cluster kernel: dynamic smem per CTA
+  int edge_cap = 0;         // cluster kernel: proposals per CTA held in smem
 };
 CommitPlan plan_commit(const DevState& d);
 cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
                           cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st);
+int commit_cluster_size(const DevState& d, size_t smem);
+cudaError_t launch_commit_cluster(const DevState& d, const CommitPlan& p, int mode,
+                                  cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st);
 // step-API helpers
 cudaError_t launch_edges_from_tables(const DevState& d, cudaStream_t st);
 cudaError_t launch_accepted_from_masks(const DevState& d, const uint8_t* agent_acc,

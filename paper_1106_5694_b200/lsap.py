@@ -435,15 +435,25 @@ class Context:
                                    float(outs[4][q])) for q in range(k.value)]
         return Assignment(s, t, v.value), applied
 
+    def counters(self) -> dict:
+        h, d, k = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(N.LIB.lsapgpu_counters(self.h, C.byref(h), C.byref(d), C.byref(k)))
+        return {"h2d_bytes": h.value, "d2h_bytes": d.value, "kernel_launches": k.value}
+
+    @property
+    def stream(self) -> int:
+        return int(N.LIB.lsapgpu_stream(self.h) or 0)
+
     def set_scan_timing(self, on: bool) -> None:
         self._check(N.LIB.lsapgpu_set_scan_timing(self.h, 1 if on else 0))
 
     def scan_timing(self) -> dict:
-        tot, fl = C.c_double(), C.c_double()
-        la, fla = C.c_int64(), C.c_int64()
-        self._check(N.LIB.lsapgpu_scan_timing(self.h, C.byref(tot), C.byref(la), C.byref(fl), C.byref(fla)))
+        tot, fl, cm = C.c_double(), C.c_double(), C.c_double()
+        la, fla, cl = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(N.LIB.lsapgpu_scan_timing(self.h, C.byref(tot), C.byref(la), C.byref(fl), C.byref(fla),
+                                              C.byref(cm), C.byref(cl)))
         return {"scan_ms": tot.value, "scan_launches": la.value, "full_ms": fl.value,
-                "full_launches": fla.value}
+                "full_launches": fla.value, "commit_ms": cm.value, "commit_launches": cl.value}
 
 
 _ctx_lock = threading.Lock()
