@@ -138,12 +138,12 @@ __global__ void __launch_bounds__(1024, 1)
 
 CommitPlan plan_commit(const DevState& d) {
   CommitPlan p;
-  // cluster kernel: key slice + as many 25-byte proposal slots as fit
+  // cluster kernel: key + flag slices and as many 45-byte proposal slots as fit
   const size_t budget = 220 * 1024;
   p.cluster_smem = budget;
   p.cluster = commit_cluster_size(d, budget);
   const size_t kslice = ((static_cast<size_t>(d.n) + p.cluster - 1) / p.cluster * 4 + 15) / 16 * 16;
-  const size_t cap = budget > kslice + 64 ? (budget - kslice - 64) / 25 : 0;
+  const size_t cap = budget > 2 * kslice + 64 ? (budget - 2 * kslice - 64) / 45 : 0;
   p.edge_cap = static_cast<int>(cap / 16 * 16);
   return p;
 }

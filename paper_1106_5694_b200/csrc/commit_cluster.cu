@@ -1,26 +1,31 @@
 // commit_cluster.cu -- the production commit kernel: one inner iteration of
 // the reference's batch loop (proj/src/parallel.cpp:264-335) minus the scans,
 // run by ONE thread-block cluster (16 CTAs x 1024 threads where the part
-// allows non-portable clusters, else 8) that keeps the whole conflict-check
-// state in distributed shared memory.
+// allows non-portable clusters, else 8) that keeps every per-vertex structure
+// of the conflict check in distributed shared memory.  Vertex v (agent or job
+// index) lives in CTA v % CS at slot v / CS: its LFMM key and a flag word
+// (bit 0 agent touched by a committed exchange, bit 1 agent already queued as
+// conflicted, bit 2 job's own proposal rejected).  The proposals are split in
+// contiguous chunks over the CTAs.
 //
-//   P0  control: abort tests (no active record -> inner loop done and the
-//       graph's WHILE condition is cleared; deadline; full delta log)
-//   P1  proposals -> edges (agent endpoints from the frozen sigma), chunked
-//       over the cluster's CTAs; vertex keys zeroed (keys of vertex v live in
-//       CTA v % CS at index v / CS)
-//   P2  LFMM rounds (see commit.cu for why they equal the reference's
-//       sequential reservation walk, parallel.cpp:35-76): phase A posts the
-//       edge's epoch-tagged inverted priority to both endpoint keys with
-//       DSMEM atomicMax (or rejects it when an endpoint is matched), phase B
-//       accepts the edges that hold both keys and marks the endpoints
-//       matched; a cluster barrier (~0.3 us) separates the phases
+//   P0  control, decided identically by every CTA from values the previous
+//       kernel wrote (no barrier): no active proposal -> inner loop done and
+//       the graph's WHILE condition cleared; full delta log -> host drain;
+//       deadline flag (checked at the end of the previous commit)
+//   P1  proposal endpoints (agents) from the frozen sigma/tau
+//   P2  LFMM rounds (see commit.cu for why they equal the sequential
+//       reservation walk of check_conflicts_impl, parallel.cpp:35-76):
+//       phase A posts the epoch-tagged inverted priority to both endpoint
+//       keys with DSMEM atomicMax (or rejects the edge when an endpoint is
+//       matched), phase B accepts edges that hold both keys
 //   P3  select: accepted records are zeroed and their improvement recomputed
-//       on the frozen assignment (solver_state.hpp:106-122), committed iff > eps
-//   P4  apply + delta log + touched work items, disjointness asserted
-//       (parallel.cpp:296-310)
-//   P5  conflicted work items (touched_and_conflicted) or carried edges
-//       (touched_only), parallel.cpp:312-330
+//       on the frozen assignment (solver_state.hpp:106-122), committed iff
+//       > eps; committed exchanges mark their agents touched in DSMEM (a
+//       second mark is the reference's overlap assertion, parallel.cpp:296-302)
+//   P4  apply (sigma/tau/acur), delta log, re-evaluation work items: touched
+//       pairs and, under touched_and_conflicted, every untouched conflicted
+//       proposer (parallel.cpp:312-330); each CTA reserves its log / item
+//       ranges with one global atomic
 #include <cooperative_groups.h>
 
 #include <climits>
@@ -37,45 +42,33 @@ constexpr uint32_t kMatched = 0xFFFFFFFFu;
 constexpr uint32_t kKeyShift = 18;  // priorities (slots) < 2^18
 constexpr uint32_t kRoundLimit = (1u << 14) - 2;
 constexpr int kNT = 1024;
+constexpr uint32_t kTouched = 1u, kQueued = 2u, kJobRejected = 4u;
+constexpr int32_t kNoEmit = -1;
+constexpr int32_t kJobFlagBit = 1 << 30;
 
 __device__ __forceinline__ uint32_t make_key(uint32_t round, int32_t slot) {
   return (round << kKeyShift) | (0x3FFFFu - static_cast<uint32_t>(slot));
 }
 
-// warp-aggregated append of `want` (0/1) entries to a global counter
-__device__ __forceinline__ int warp_append(int* counter, bool want) {
-  const unsigned mask = __ballot_sync(0xffffffffu, want);
-  if (!mask) return -1;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(mask) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(counter, __popc(mask));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  return want ? base + __popc(mask & ((1u << lane) - 1)) : -1;
-}
-__device__ __forceinline__ long long warp_append64(long long* counter, bool want) {
-  const unsigned mask = __ballot_sync(0xffffffffu, want);
-  if (!mask) return -1;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(mask) - 1;
-  unsigned long long base = 0;
-  if (lane == leader)
-    base = atomicAdd(reinterpret_cast<unsigned long long*>(counter), static_cast<unsigned long long>(__popc(mask)));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  return want ? static_cast<long long>(base) + __popc(mask & ((1u << lane) - 1)) : -1;
-}
-
-__device__ __forceinline__ int block_sum(int v, int* s) {
+__device__ __forceinline__ void block_add(int v, int* s) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(s, v);
-  return v;
 }
 
 struct CommitScratch {  // per-CTA shared scalars
-  int abort;
   int count[2];
-  int committed, ascans, jscans, items;
   int total;
+  int nlog, nconf, nconf_j;
+  unsigned long long base_log;
+  int base_items;
+};
+
+// Per-proposal working set of this CTA (shared memory, or global scratch
+// when the chunk does not fit).
+struct EdgeArrays {
+  int32_t *u, *v, *jold, *rank, *slot;
+  uint8_t* st;
+  double *del, *acur_a, *acur_d;
 };
 
 template <class E, int CS>
@@ -88,6 +81,7 @@ __global__ void __launch_bounds__(kNT, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CommitScratch sc;
   __shared__ uint32_t* kbase[CS];
+  __shared__ uint32_t* fbase[CS];
 
   Ctrl* C = st.ctrl;
   const int32_t n = st.n;
@@ -98,81 +92,93 @@ __global__ void __launch_bounds__(kNT, 1)
   const int32_t m = C->edge_count[P];
   const int4* edges = st.edges[P];
 
-  // ---- P0: control (rank 0 decides, everyone reads its verdict) ----
-  if (tid == 0) {
-    sc.abort = 0;
-    sc.count[0] = sc.count[1] = 0;
-    sc.committed = sc.ascans = sc.jscans = sc.items = 0;
-    if (rank == 0 && mode == kCommitSolve) {
-      if (C->expired || C->drain || C->error || C->inner_done)
-        sc.abort = 1;
-      else if (m == 0)
-        sc.abort = 2;
-      else if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt)
-        sc.abort = 3;
-      else if (C->log_count + m > st.log_cap)
-        sc.abort = 4;
+  // ---- P0: control ----
+  if (mode == kCommitSolve) {
+    int abort = 0;
+    if (C->expired || C->drain || C->error || C->inner_done)
+      abort = 1;
+    else if (m == 0)
+      abort = 2;
+    else if (C->log_count + m > st.log_cap)
+      abort = 4;
+    if (abort) {
+      if (rank == 0 && tid == 0) {
+        if (abort == 2) C->inner_done = 1;
+        if (abort == 4) C->drain = 1;
+        C->work_count = 0;
+        if (use_cond) cudaGraphSetConditional(cond, 0);
+      }
+      return;
     }
-  }
-  if (tid < CS) kbase[tid] = cluster.map_shared_rank(reinterpret_cast<uint32_t*>(smem), tid);
-  cluster.sync();
-  const int abort = *cluster.map_shared_rank(&sc.abort, 0);
-  cluster.sync();  // rank 0's shared memory must outlive every peer read
-  if (abort) {
-    if (rank == 0 && tid == 0) {
-      if (abort == 2) C->inner_done = 1;
-      if (abort == 3) C->expired = 1;
-      if (abort == 4) C->drain = 1;
-      C->work_count = 0;
-      if (use_cond) cudaGraphSetConditional(cond, 0);
-    }
-    return;
+    if (rank == 0 && tid == 0) C->work_count = 0;  // appends start after two cluster barriers
   }
   const int32_t iter = C->iter + 1;
-  if (rank == 0 && tid == 0) C->work_count = 0;  // nobody appends before the next cluster barrier
 
-  // ---- P1: keys and this CTA's edges ----
+  // ---- P1: vertex slices, proposal endpoints ----
   const int32_t kslice = (n + CS - 1) / CS;
+  const size_t kbytes = ((static_cast<size_t>(kslice) * 4 + 15) / 16) * 16;
   uint32_t* mykeys = reinterpret_cast<uint32_t*>(smem);
-  for (int32_t x = tid; x < kslice; x += kNT) mykeys[x] = 0u;
+  uint32_t* myflags = reinterpret_cast<uint32_t*>(smem + kbytes);
+  if (tid < CS) {
+    kbase[tid] = cluster.map_shared_rank(mykeys, tid);
+    fbase[tid] = cluster.map_shared_rank(myflags, tid);
+  }
+  if (tid == 0) {
+    sc.count[0] = sc.count[1] = 0;
+    sc.nlog = sc.nconf = sc.nconf_j = 0;
+  }
+  for (int32_t x = tid; x < kslice; x += kNT) {
+    mykeys[x] = 0u;
+    myflags[x] = 0u;
+  }
   const int32_t per = (m + CS - 1) / CS;
   const int32_t e0 = rank * per;
   const int32_t cnt = max(0, min(m, e0 + per) - e0);
-  int32_t *Eu, *Ev, *Ejold, *Ejnew;
-  uint8_t* Est;
-  double* Edel;
+  EdgeArrays Ea;
   if (per <= edge_cap) {
-    unsigned char* q = smem + ((static_cast<size_t>(kslice) * 4 + 15) / 16) * 16;
-    Edel = reinterpret_cast<double*>(q);
+    unsigned char* q = smem + 2 * kbytes;
+    Ea.del = reinterpret_cast<double*>(q);
     q += static_cast<size_t>(edge_cap) * 8;
-    Eu = reinterpret_cast<int32_t*>(q);
+    Ea.acur_a = reinterpret_cast<double*>(q);
+    q += static_cast<size_t>(edge_cap) * 8;
+    Ea.acur_d = reinterpret_cast<double*>(q);
+    q += static_cast<size_t>(edge_cap) * 8;
+    Ea.u = reinterpret_cast<int32_t*>(q);
     q += static_cast<size_t>(edge_cap) * 4;
-    Ev = reinterpret_cast<int32_t*>(q);
+    Ea.v = reinterpret_cast<int32_t*>(q);
     q += static_cast<size_t>(edge_cap) * 4;
-    Ejold = reinterpret_cast<int32_t*>(q);
+    Ea.jold = reinterpret_cast<int32_t*>(q);
     q += static_cast<size_t>(edge_cap) * 4;
-    Ejnew = reinterpret_cast<int32_t*>(q);
+    Ea.rank = reinterpret_cast<int32_t*>(q);
     q += static_cast<size_t>(edge_cap) * 4;
-    Est = q;
-  } else {  // too many proposals for DSMEM: same layout in global scratch
-    Eu = st.eu + e0;
-    Ev = st.ev + e0;
-    Ejold = st.eprop + e0;
-    Ejnew = st.c_jnew + e0;
-    Est = st.estate + e0;
-    Edel = st.c_delta + e0;
+    Ea.slot = reinterpret_cast<int32_t*>(q);
+    q += static_cast<size_t>(edge_cap) * 4;
+    Ea.st = q;
+  } else {  // too many proposals for shared memory: same arrays in global scratch
+    Ea.del = st.c_delta + e0;
+    Ea.acur_a = st.c_acur + e0;
+    Ea.acur_d = st.c_acur + 2 * static_cast<int64_t>(n) + e0;
+    Ea.u = st.eu + e0;
+    Ea.v = st.ev + e0;
+    Ea.jold = st.eprop + e0;
+    Ea.rank = st.c_rank + e0;
+    Ea.slot = st.c_jnew + e0;
+    Ea.st = st.estate + e0;
   }
   for (int32_t l = tid; l < cnt; l += kNT) {
     // proposals carry {slot, proposer, partner, job}: one dependent load left
     const int4 en = edges[e0 + l];
-    Eu[l] = en.y;  // proposer: the agent, or the job's current holder (frozen)
+    Ea.u[l] = en.y;  // proposer: the agent, or the job's current holder (frozen)
     if (en.x < n) {
-      Ev[l] = st.sigma[en.z];  // the displaced holder of the proposed job
+      Ea.v[l] = st.sigma[en.z];  // the displaced holder of the proposed job
+      Ea.jold[l] = en.w;         // the proposer's current job
     } else {
-      Ev[l] = en.z;                 // the proposed agent
-      Ejold[l] = st.tau[en.z];      // ... and its current job
+      Ea.v[l] = en.z;             // the proposed agent
+      Ea.jold[l] = st.tau[en.z];  // ... and its current job
     }
-    Est[l] = kEdgeUndecided;
+    Ea.st[l] = kEdgeUndecided;
+    Ea.rank[l] = kNoEmit;
+    Ea.slot[l] = en.x;
   }
   cluster.sync();
 
@@ -188,38 +194,38 @@ __global__ void __launch_bounds__(kNT, 1)
     }
     int local = 0;
     for (int32_t l = tid; l < cnt; l += kNT) {
-      if (Est[l] != kEdgeUndecided) continue;
-      const int32_t u = Eu[l], v = Ev[l];
+      if (Ea.st[l] != kEdgeUndecided) continue;
+      const int32_t u = Ea.u[l], v = Ea.v[l];
       uint32_t* ku = kbase[u % CS] + u / CS;
       uint32_t* kv = kbase[v % CS] + v / CS;
       if (*ku == kMatched || *kv == kMatched) {
-        Est[l] = kEdgeRejected;
+        Ea.st[l] = kEdgeRejected;
       } else {
-        const uint32_t k = make_key(R, edges[e0 + l].x);
+        const uint32_t k = make_key(R, Ea.slot[l]);
         atomicMax(ku, k);
         atomicMax(kv, k);
         ++local;
       }
     }
-    block_sum(local, &sc.count[rounds & 1]);
+    block_add(local, &sc.count[rounds & 1]);
     cluster.sync();
     if (tid == 0) {
       int tot = 0;
+#pragma unroll
       for (int r = 0; r < CS; ++r) tot += *cluster.map_shared_rank(&sc.count[rounds & 1], r);
       sc.total = tot;
+      sc.count[(rounds + 1) & 1] = 0;  // peers read it only after the next cluster barrier
     }
     __syncthreads();
-    const int total = sc.total;
-    if (tid == 0) sc.count[(rounds + 1) & 1] = 0;  // read by peers only after the next barrier
-    if (total == 0) break;
+    if (sc.total == 0) break;
     for (int32_t l = tid; l < cnt; l += kNT) {
-      if (Est[l] != kEdgeUndecided) continue;
-      const int32_t u = Eu[l], v = Ev[l];
+      if (Ea.st[l] != kEdgeUndecided) continue;
+      const int32_t u = Ea.u[l], v = Ea.v[l];
       uint32_t* ku = kbase[u % CS] + u / CS;
       uint32_t* kv = kbase[v % CS] + v / CS;
-      const uint32_t k = make_key(R, edges[e0 + l].x);
+      const uint32_t k = make_key(R, Ea.slot[l]);
       if (*ku == k && *kv == k) {
-        Est[l] = kEdgeAccepted;
+        Ea.st[l] = kEdgeAccepted;
         *ku = kMatched;
         *kv = kMatched;
       }
@@ -232,146 +238,135 @@ __global__ void __launch_bounds__(kNT, 1)
   if (mode == kCommitCheckOnly) {
     if (per <= edge_cap)
       for (int32_t l = tid; l < cnt; l += kNT) {
-        st.estate[e0 + l] = Est[l];
-        st.eu[e0 + l] = Eu[l];
-        st.ev[e0 + l] = Ev[l];
+        st.estate[e0 + l] = Ea.st[l];
+        st.eu[e0 + l] = Ea.u[l];
+        st.ev[e0 + l] = Ea.v[l];
       }
-    if (rank == 0 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&C->lfmm_rounds),
-                                         static_cast<unsigned long long>(rounds));
-    cluster.sync();  // keep peer smem alive until everyone is done
+    if (rank == 0 && tid == 0) C->lfmm_rounds += rounds;
+    cluster.sync();  // peers may still read our counters
     return;
   }
 
-  // ---- P3: select (frozen reads) ----
+  // ---- P3: select on the frozen assignment; mark touched / rejected ----
   const double eps = st.eps;
+  int overlap = 0;
   for (int32_t l = tid; l < cnt; l += kNT) {
-    if (Est[l] != kEdgeAccepted) continue;
+    const uint8_t s = Ea.st[l];
+    if (s == kEdgeRejected) {
+      const int4 en = edges[e0 + l];
+      if (en.x >= n) atomicOr(fbase[en.w % CS] + en.w / CS, kJobRejected);
+      continue;
+    }
+    if (s != kEdgeAccepted) continue;
     const int4 en = edges[e0 + l];
-    int32_t agent, j_new, j_old, disp;
-    typename Traits<E>::Acc actual;
+    int32_t agent, j_new, disp;
+    const int32_t j_old = Ea.jold[l];
     if (en.x < n) {  // agent_proposal_delta, solver_state.hpp:106-113
       agent = en.y;
       j_new = en.z;
-      j_old = en.w;
-      disp = Ev[l];
+      disp = Ea.v[l];
       st.agent_delta[agent] = 0.0;
       st.agent_partner[agent] = -1;
-      const int64_t ra = static_cast<int64_t>(agent) * ld, rd = static_cast<int64_t>(disp) * ld;
-      actual = delta4(widen(A[ra + j_new]), widen(A[ra + j_old]), widen(A[rd + j_old]),
-                      widen(A[rd + j_new]));
-    } else {  // job_proposal_delta, solver_state.hpp:115-122
+    } else {  // job_proposal_delta, solver_state.hpp:115-122 (i_new = agent, holder = disp)
       agent = en.z;
       j_new = en.w;
       disp = en.y;
-      j_old = Ejold[l];
       st.job_delta[j_new] = 0.0;
       st.job_partner[j_new] = -1;
-      const int64_t ri = static_cast<int64_t>(agent) * ld, rh = static_cast<int64_t>(disp) * ld;
-      actual = delta4(widen(A[ri + j_new]), widen(A[rh + j_new]), widen(A[rh + j_old]),
-                      widen(A[ri + j_old]));
     }
-    const double dact = static_cast<double>(actual);
+    const int64_t ra = static_cast<int64_t>(agent) * ld, rd = static_cast<int64_t>(disp) * ld;
+    const auto a_new = widen(A[ra + j_new]), a_old = widen(A[ra + j_old]);
+    const auto d_old = widen(A[rd + j_old]), d_new = widen(A[rd + j_new]);
+    const double dact = en.x < n ? static_cast<double>(delta4(a_new, a_old, d_old, d_new))
+                                 : static_cast<double>(delta4(a_new, d_new, d_old, a_old));
     if (dact > eps) {
-      Est[l] = kEdgeCommitted;
-      Eu[l] = agent;
-      Ev[l] = disp;
-      Ejold[l] = j_old;
-      Ejnew[l] = j_new;
-      Edel[l] = dact;
+      Ea.st[l] = kEdgeCommitted;
+      Ea.u[l] = agent;
+      Ea.v[l] = disp;
+      Ea.jold[l] = j_old;
+      Ea.del[l] = dact;
+      Ea.acur_a[l] = static_cast<double>(a_new);
+      Ea.acur_d[l] = static_cast<double>(d_old);
+      const uint32_t o1 = atomicOr(fbase[agent % CS] + agent / CS, kTouched);
+      const uint32_t o2 = atomicOr(fbase[disp % CS] + disp / CS, kTouched);
+      if ((o1 | o2) & kTouched) overlap = 1;
     }
   }
+  if (overlap) atomicExch(&C->error, 1);
   cluster.sync();
 
-  // ---- P4: apply, log, touched work items ----
-  int committed = 0;
-  for (int32_t base = 0; base < cnt; base += kNT) {  // warp-uniform trip count for the appends
-    const int32_t l = base + tid;
-    const bool mine = l < cnt && Est[l] == kEdgeCommitted;
-    int32_t agent = 0, disp = 0;
-    if (mine) {
-      agent = Eu[l];
-      disp = Ev[l];
-      const int32_t j_old = Ejold[l], j_new = Ejnew[l];
-      if (atomicExch(&st.touched_stamp[agent], iter) == iter ||
-          atomicExch(&st.touched_stamp[disp], iter) == iter)
-        atomicExch(&C->error, 1);
+  // ---- P4: apply, then rank log entries and work items ----
+  for (int32_t l = tid; l < cnt; l += kNT) {
+    const uint8_t s = Ea.st[l];
+    if (s == kEdgeCommitted) {
+      const int32_t agent = Ea.u[l], disp = Ea.v[l], j_old = Ea.jold[l];
+      const int4 en = edges[e0 + l];
+      const int32_t j_new = en.x < n ? en.z : en.w;
       st.sigma[j_new] = agent;
       st.sigma[j_old] = disp;
       st.tau[agent] = j_new;
       st.tau[disp] = j_old;
-      acur[agent] = A[static_cast<int64_t>(agent) * ld + j_new];
-      acur[disp] = A[static_cast<int64_t>(disp) * ld + j_old];
-      ++committed;
-    }
-    const long long pos = warp_append64(reinterpret_cast<long long*>(&C->log_count), mine);
-    if (mine) st.log[pos] = LogEntry{iter, edges[e0 + l].x, Edel[l]};
-    const unsigned mask = __ballot_sync(0xffffffffu, mine);
-    if (mask) {
-      const int lane = tid & 31;
-      const int leader = __ffs(mask) - 1;
-      int w = 0;
-      if (lane == leader) w = atomicAdd(&C->work_count, 2 * __popc(mask));
-      w = __shfl_sync(0xffffffffu, w, leader);
-      if (mine) {
-        const int o = w + 2 * __popc(mask & ((1u << lane) - 1));
-        st.items[o] = static_cast<uint32_t>(agent) | kItemAgent | kItemJob;
-        st.items[o + 1] = static_cast<uint32_t>(disp) | kItemAgent | kItemJob;
-      }
-    }
-  }
-  block_sum(committed, &sc.committed);
-  for (int32_t l = tid; l < cnt; l += kNT)
-    if (Est[l] == kEdgeRejected) st.rej_stamp[edges[e0 + l].x] = iter;
-  cluster.sync();
-
-  // ---- P5: conflicted re-evaluation / carried edges ----
-  int la = 0, lj = 0;
-  for (int32_t base = 0; base < cnt; base += kNT) {
-    const int32_t l = base + tid;
-    bool emit = false, jflag = false;
-    int32_t p = 0;
-    if (l < cnt && Est[l] == kEdgeRejected) {
+      acur[agent] = static_cast<E>(Ea.acur_a[l]);
+      acur[disp] = static_cast<E>(Ea.acur_d[l]);
+      Ea.rank[l] = atomicAdd(&sc.nlog, 1);
+    } else if (s == kEdgeRejected) {
       const int4 en = edges[e0 + l];
-      p = en.y;  // the proposer (frozen holder for job-side proposals)
+      const int32_t p = en.y;  // the proposer (frozen holder for job-side proposals)
+      uint32_t* fp = fbase[p % CS] + p / CS;
       if (st.policy == 0) {
-        if (st.touched_stamp[p] != iter && atomicExch(&st.conf_stamp[p], iter) != iter) {
-          // p is untouched, so its job is still the proposal's job (en.w for
-          // job records, tau[p] = en.w for agent records as well)
-          jflag = st.rej_stamp[n + en.w] == iter;
-          emit = true;
-          ++la;
-          if (jflag) ++lj;
+        if (!(*fp & kTouched) && !(atomicOr(fp, kQueued) & kQueued)) {
+          // p is untouched, so its job is still the proposal's job en.w
+          const bool jflag = (fbase[en.w % CS][en.w / CS] & kJobRejected) != 0;
+          Ea.rank[l] = atomicAdd(&sc.nconf, 1) | (jflag ? kJobFlagBit : 0);
+          if (jflag) atomicAdd(&sc.nconf_j, 1);
         }
-      } else if (st.touched_stamp[p] != iter) {
+      } else if (!(*fp & kTouched)) {
         // touched_only: an untouched proposer keeps its stale record -> carry it
         const int pos = atomicAdd(&C->edge_count[1 - P], 1);
         st.edges[1 - P][pos] = en;
       }
     }
-    const int w = warp_append(&C->work_count, emit);
-    if (emit) st.items[w] = static_cast<uint32_t>(p) | kItemAgent | (jflag ? kItemJob : 0u);
   }
-  block_sum(la, &sc.ascans);
-  block_sum(lj, &sc.jscans);
   __syncthreads();
   if (tid == 0) {
-    const long long touched = 2ll * sc.committed;
-    atomicAdd(reinterpret_cast<unsigned long long*>(&C->switches), static_cast<unsigned long long>(sc.committed));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&C->agent_scans),
-              static_cast<unsigned long long>(touched + sc.ascans));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&C->job_scans),
-              static_cast<unsigned long long>(touched + sc.jscans));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&C->pair_items),
-              static_cast<unsigned long long>(touched + sc.ascans));
+    const int nlog = sc.nlog, nitems = 2 * sc.nlog + sc.nconf;
+    sc.base_log = nlog ? atomicAdd(reinterpret_cast<unsigned long long*>(&C->log_count),
+                                   static_cast<unsigned long long>(nlog))
+                       : 0ull;
+    sc.base_items = nitems ? atomicAdd(&C->work_count, nitems) : 0;
+    if (nlog) atomicAdd(reinterpret_cast<unsigned long long*>(&C->switches), static_cast<unsigned long long>(nlog));
+    if (nitems) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C->pair_items), static_cast<unsigned long long>(nitems));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C->agent_scans), static_cast<unsigned long long>(nitems));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C->job_scans),
+                static_cast<unsigned long long>(2 * sc.nlog + sc.nconf_j));
+    }
   }
-  cluster.sync();  // all appends done, peer smem no longer referenced
+  __syncthreads();
+  const unsigned long long blog = sc.base_log;
+  const int bitems = sc.base_items, nlog2 = 2 * sc.nlog;
+  for (int32_t l = tid; l < cnt; l += kNT) {
+    const int32_t r = Ea.rank[l];
+    if (r == kNoEmit) continue;
+    if (Ea.st[l] == kEdgeCommitted) {
+      st.log[blog + r] = LogEntry{iter, edges[e0 + l].x, Ea.del[l]};
+      st.items[bitems + 2 * r] = static_cast<uint32_t>(Ea.u[l]) | kItemAgent | kItemJob;
+      st.items[bitems + 2 * r + 1] = static_cast<uint32_t>(Ea.v[l]) | kItemAgent | kItemJob;
+    } else {
+      const int32_t p = edges[e0 + l].y;
+      st.items[bitems + nlog2 + (r & ~kJobFlagBit)] =
+          static_cast<uint32_t>(p) | kItemAgent | ((r & kJobFlagBit) ? kItemJob : 0u);
+    }
+  }
+  cluster.sync();  // every peer is done with this CTA's shared memory
   if (rank == 0 && tid == 0) {
     C->iter = iter;
-    C->round = 1;
     C->parity = 1 - P;
     C->edge_count[P] = 0;
     C->lfmm_rounds += rounds;
     C->inner_iterations += 1;
+    // anytime deadline, acted on by the next commit (solver_state.hpp:13-27)
+    if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
   }
 }
 

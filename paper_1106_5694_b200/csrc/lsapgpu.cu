@@ -178,6 +178,9 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.estate, N2, false));
   CK(valloc(ctx, &d.c_jnew, N2, false));
   CK(valloc(ctx, &d.c_delta, N2, false));
+  CK(valloc(ctx, &d.c_acur, 2 * N2, false));
+  CK(valloc(ctx, &d.c_rank, N2, false));
+  CK(valloc(ctx, &d.vstate, N, true));
   CK(valloc(ctx, &d.keys, N, true));
   CK(valloc(ctx, &d.touched_stamp, N, true));
   CK(valloc(ctx, &d.conf_stamp, N, true));
@@ -322,6 +325,29 @@ int run_scan(lsapgpu_ctx* ctx, int full) {
     }
   }
   return LSAPGPU_OK;
+}
+
+// Stable two-pass counting sort of the delta log by (iter, slot): O(entries + slots).
+void order_log(const std::vector<LogEntry>& in, std::vector<LogEntry>& out, int32_t slots) {
+  const size_t N = in.size();
+  out.resize(N);
+  if (N == 0) return;
+  static thread_local std::vector<LogEntry> tmp;
+  static thread_local std::vector<int64_t> count;
+  tmp.resize(N);
+  count.assign(static_cast<size_t>(slots) + 1, 0);
+  for (const auto& e : in) ++count[static_cast<size_t>(e.slot) + 1];
+  for (size_t k = 1; k < count.size(); ++k) count[k] += count[k - 1];
+  for (const auto& e : in) tmp[static_cast<size_t>(count[e.slot]++)] = e;
+  int32_t lo = tmp[0].iter, hi = tmp[0].iter;
+  for (const auto& e : tmp) {
+    lo = std::min(lo, e.iter);
+    hi = std::max(hi, e.iter);
+  }
+  count.assign(static_cast<size_t>(hi - lo) + 2, 0);
+  for (const auto& e : tmp) ++count[static_cast<size_t>(e.iter - lo) + 1];
+  for (size_t k = 1; k < count.size(); ++k) count[k] += count[k - 1];
+  for (const auto& e : tmp) out[static_cast<size_t>(count[e.iter - lo]++)] = e;
 }
 
 struct TraceSink {
@@ -774,7 +800,7 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   rc = pull_ctrl(ctx);
   if (rc) return rc;
   const Ctrl base = *ctx->ctrl_host;  // counters are cumulative per context
-  std::vector<LogEntry> log;
+  std::vector<LogEntry> log, sorted;
   int64_t switches = 0;
   int64_t launches = 0;
   int64_t graph_launches = 0;
@@ -831,11 +857,13 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
         CK(cpy(ctx, log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
       }
-      // batch order: iteration, then ascending slot (agents then jobs)
-      std::sort(log.begin(), log.end(), [](const LogEntry& a, const LogEntry& b) {
-        return a.iter != b.iter ? a.iter < b.iter : a.slot < b.slot;
-      });
-      for (const auto& L : log) {
+      // Replay in the reference's batch order (iteration, then ascending slot:
+      // agents then jobs, parallel.cpp:306-310).  Integer deltas sum exactly in
+      // any order, so without a trace the order only matters for float storage.
+      const bool need_order = (trace_switch && trace_value) || d.storage == kF32 || d.storage == kF64;
+      if (need_order) order_log(log, sorted, 2 * n);
+      const std::vector<LogEntry>& seq = need_order ? sorted : log;
+      for (const auto& L : seq) {
         value += L.delta;
         ++switches;
         trace.push(switches, value);

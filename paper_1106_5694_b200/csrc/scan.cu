@@ -275,7 +275,7 @@ constexpr int kEdgeBuf = 512;
 constexpr int kMaxBufs = 4;
 
 template <class E, int M, int NT, int KM, bool kChunked>
-__global__ void __launch_bounds__(NT, 1) pair_scan_kernel(DevState st, int full, int passes,
+__global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, int full, int passes,
                                                           int64_t chunk, int bufs, int max_segments) {
   using Acc = typename Traits<E>::Acc;
   constexpr int V = StreamRegs<E, M>::V;
@@ -581,17 +581,21 @@ __global__ void __launch_bounds__(NT, 1) pair_scan_kernel(DevState st, int full,
   for (int e = tid; e < ne; e += NT) st.edges[parity_out][gbase + e] = ebuf[e];
 }
 
-constexpr int kThreads = 512;
+constexpr size_t kStaticSmem = 9 * 1024;  // ebuf + item metadata + counters (+ slack)
 
-template <class E, int M, int KM>
-cudaError_t launch_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  auto k = p.passes > 1 ? pair_scan_kernel<E, M, kThreads, KM, true>
-                        : pair_scan_kernel<E, M, kThreads, KM, false>;
+template <class E, int M, int NT, int KM>
+cudaError_t launch_nt(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  auto k = p.passes > 1 ? pair_scan_kernel<E, M, NT, KM, true> : pair_scan_kernel<E, M, NT, KM, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;
-  k<<<p.ctas, kThreads, p.smem, st>>>(d, full, p.passes, p.chunk, p.bufs, p.max_segments);
+  k<<<p.ctas, NT, p.smem, st>>>(d, full, p.passes, p.chunk, p.bufs, p.max_segments);
   return cudaGetLastError();
+}
+
+template <class E, int M, int KM>
+cudaError_t launch_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  return p.threads == 256 ? launch_nt<E, M, 256, KM>(d, p, full, st) : launch_nt<E, M, 512, KM>(d, p, full, st);
 }
 
 template <class E, int KM>
@@ -627,26 +631,34 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
   if (const char* m = std::getenv("LSAPGPU_SCAN_M")) force_m = std::atoi(m);
   const size_t row = static_cast<size_t>(d.ld) * es;
   const size_t reserve = 256 + 4 * 16 * 8 * 16;  // barriers + reduction scratch (B x NW x 2M tracks)
-  p.threads = kThreads;
+  p.threads = 512;
   int force_bufs = 0;
   if (const char* bb = std::getenv("LSAPGPU_SCAN_BUFS")) force_bufs = std::atoi(bb);
+  // Two co-resident 256-thread CTAs per SM, single-buffered, interleave their
+  // staging and compute better than one double-buffered CTA (measured on
+  // B200, n=10k: int16 3.9 vs 3.4 TB/s full sweep, fp32 3.7 vs 3.1).  Batch
+  // as many items per stage as still allows two CTAs per SM.
+  const size_t two_cta = (227 * 1024) / 2 - kStaticSmem - 1024 - reserve;
   if (row <= budget) {
     p.passes = 1;
     p.chunk = d.ld;
-    // batch items (tau/acur stream shared by M rows) while keeping >= 3 stages
-    // of staged rows in flight; fall back to fewer stages for long rows
-    p.m = 1;
+    p.bufs = 1;
+    p.m = 0;
     for (int m : {4, 2, 1})
-      if (static_cast<size_t>(m) * 3 * row <= budget) {
+      if (static_cast<size_t>(m) * row <= two_cta) {
         p.m = m;
         break;
       }
+    if (p.m == 0) {  // one row per CTA does not fit twice: one 512-thread CTA per SM
+      p.m = 1;
+      p.threads = 512;
+    } else {
+      p.threads = 256;
+    }
     if (force_m == 1 || force_m == 2 || force_m == 4) p.m = force_m;
-    p.bufs = static_cast<int>(budget / (static_cast<size_t>(p.m) * row));
-    if (p.bufs > 4) p.bufs = 4;
     if (force_bufs >= 1 && force_bufs <= 4 && static_cast<size_t>(force_bufs) * p.m * row <= budget)
       p.bufs = force_bufs;
-    if (p.bufs < 1) p.bufs = 1;
+    if (const char* t = std::getenv("LSAPGPU_SCAN_NT")) p.threads = std::atoi(t) == 256 ? 256 : 512;
   } else {
     p.m = 1;
     p.bufs = 1;
@@ -656,9 +668,9 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     p.chunk = ch;
   }
   p.smem = static_cast<size_t>(p.bufs) * p.m * p.chunk * es + reserve;
-  int per_sm = static_cast<int>((227 * 1024) / (p.smem + 1024));
+  int per_sm = static_cast<int>((227 * 1024) / (p.smem + kStaticSmem + 1024));
   if (per_sm < 1) per_sm = 1;
-  if (per_sm > 4) per_sm = 4;  // 512-thread CTAs: at most 4 per SM
+  if (per_sm > 512 / p.threads) per_sm = 512 / p.threads;  // register budget: 512 threads per SM
   p.ctas = num_sms * per_sm;
   p.max_segments = static_cast<int>(d.n / 2048);
   if (p.max_segments < 1) p.max_segments = 1;

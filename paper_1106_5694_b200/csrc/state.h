@@ -40,6 +40,9 @@ struct DevState {
   uint8_t* estate = nullptr;               // edge state
   int32_t* c_jnew = nullptr;               // committed exchange: new job
   double* c_delta = nullptr;               // committed exchange: recomputed delta
+  double* c_acur = nullptr;                // committed exchange: new acur of agent / displaced (2 x 2n)
+  int32_t* c_rank = nullptr;               // per-proposal append rank (cluster commit, global fallback)
+  uint32_t* vstate = nullptr;              // per-vertex flags (cluster commit, global fallback)
   uint32_t* keys = nullptr;                // vertex keys when they do not fit in smem
   int32_t* touched_stamp = nullptr;        // agent touched in iteration k
   int32_t* conf_stamp = nullptr;           // agent queued as conflicted in iteration k

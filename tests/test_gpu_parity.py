@@ -115,6 +115,8 @@ def test_generators_match_oracle(oracle, gpu_ctx):
     {"LSAPGPU_SCAN_BUDGET": "3072"},                                   # 4 passes, single buffer
     {"LSAPGPU_SCAN_BUDGET": "9000", "LSAPGPU_SCAN_M": "1"},            # single-buffered rows
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # split items over CTAs
+    {"LSAPGPU_SCAN_NT": "512", "LSAPGPU_SCAN_BUFS": "2"},               # double-buffered ring
+    {"LSAPGPU_SCAN_NT": "512", "LSAPGPU_SCAN_BUFS": "4", "LSAPGPU_SCAN_M": "1"},  # 4-deep ring
 ])
 def test_scan_plan_variants_subprocess(env):
     """Every scan-plan code path (batching, chunked passes, segments) is bit-exact.
