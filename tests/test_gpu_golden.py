@@ -1,0 +1,93 @@
+"""GPU suite against the golden fixtures the reference itself produced
+(tests/golden/make_golden.py): every BASELINE config -- C1 int 1k, C2 int 5k,
+C3 P2P 10k, fp32 10k, int 10k, C4 fp32 30k -- generated on the device with the
+same splitmix64 recipes and solved through the C-ABI; sigma, tau, the value
+bits, outer iterations, switches and the objective trace must be identical."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "golden.json")))
+ARR = np.load(os.path.join(HERE, "golden", "small_cases.npz"))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def trace_sha(trace):
+    sw = np.array([t[0] for t in trace], np.int64)
+    va = np.array([t[1] for t in trace], np.float64)
+    return hashlib.sha256(sw.tobytes() + va.tobytes()).hexdigest()
+
+
+def cfg(rec, **kw):
+    import paper_1106_5694_b200 as g
+    return g.ParallelConfig(seed=rec["seed"], improvement_epsilon=rec["eps"],
+                            reeval="touched_only" if rec["policy"] else "touched_and_conflicted", **kw)
+
+
+def check(rep, rec):
+    assert sha(rep.assignment.sigma) == rec["sigma_sha"]
+    assert sha(rep.assignment.tau) == rec["tau_sha"]
+    assert float(rep.assignment.value).hex() == rec["value_hex"]
+    assert rep.outer_iterations == rec["outer"]
+    assert rep.switches_applied == rec["switches"]
+    assert rep.terminated_by == rec["terminated_by"]
+    assert len(rep.objective_trace) == rec["trace_len"]
+    assert trace_sha(rep.objective_trace) == rec["trace_sha"]
+
+
+@pytest.mark.parametrize("name", sorted(GOLD["solves"]))
+def test_config_solves_bit_exact_vs_reference(gpu_ctx, name):
+    rec = GOLD["solves"][name]
+    gpu_ctx.generate(rec["kind"], rec["n"], rec["instance_seed"], rec["param"])
+    check(gpu_ctx.solve(cfg(rec)), rec)
+
+
+@pytest.mark.parametrize("name", sorted(GOLD["small"]))
+@pytest.mark.parametrize("graph", [True, False])
+def test_small_solves_bit_exact_vs_reference(oracle, gpu_ctx, name, graph):
+    rec = GOLD["small"][name]
+    if rec["kind"] == "explicit2":
+        a = np.array([[0.0, 10.0], [10.0, 0.0]])
+    else:
+        a = oracle.generate(rec["kind"], rec["n"], rec["instance_seed"], rec["param"])
+    gpu_ctx.set_matrix(a)
+    rep = gpu_ctx.solve(cfg(rec, use_graph=graph))
+    check(rep, rec)
+    assert np.array_equal(rep.assignment.sigma, ARR[name + "__sigma"])
+
+
+@pytest.mark.parametrize("key", sorted(GOLD["steps"]))
+def test_step_apis_vs_reference(oracle, gpu_ctx, key):
+    import paper_1106_5694_b200 as g
+    rec = GOLD["steps"][key]
+    n = rec["n"]
+    a = oracle.generate(rec["kind"], n, rec["seed"])
+    sigma = oracle.random_perm(n, rec["sigma_seed"])
+    gpu_ctx.set_matrix(a)
+    t = gpu_ctx.evaluate_all(sigma)
+    for nm, v in (("ad", t.agent_delta), ("ap", t.agent_partner), ("jd", t.job_delta), ("jp", t.job_partner)):
+        assert np.array_equal(np.asarray(v).view(np.uint8), ARR[f"{key}__{nm}"].view(np.uint8)), nm
+    sets = gpu_ctx.check_conflicts(t, sigma)
+    assert np.array_equal(sets.agent_accepted, ARR[f"{key}__acc_a"])
+    assert np.array_equal(sets.job_accepted, ARR[f"{key}__acc_j"])
+    assert sets.reserved == np.flatnonzero(ARR[f"{key}__reserved"]).tolist()
+    assert sets.conflicted == np.flatnonzero(ARR[f"{key}__conflicted"]).tolist()
+    assert sets.conflicted_jobs == ARR[f"{key}__cjobs"].tolist()
+    gpu_ctx.set_matrix(a)  # check_conflicts may reuse the vectors
+    tau = np.empty(n, np.int32)
+    tau[sigma] = np.arange(n)
+    value = float(np.cumsum(a[sigma, np.arange(n)])[-1])
+    out, applied = gpu_ctx.apply_parallel_switches(g.Assignment(sigma, tau, value), t, sets)
+    assert np.array_equal(out.sigma, ARR[f"{key}__sigma_after"])
+    assert float(out.value).hex() == rec["value_after_hex"]
+    assert [[x.agent, x.new_job, x.old_job, x.displaced] for x in applied] == ARR[f"{key}__applied"].tolist()
+    assert [x.delta for x in applied] == ARR[f"{key}__applied_delta"].tolist()
