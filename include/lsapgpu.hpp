@@ -1,0 +1,196 @@
+// lsapgpu.hpp -- header-only C++ wrapper that puts the B200 solver behind the
+// reference's own C++ types and entry points.
+//
+// Include it AFTER the reference headers (it uses lsap::Instance, Assignment,
+// DeltaTables, ConflictSets, AppliedExchange, ParallelConfig, SolveReport and
+// lsap::Error from proj/include/lsap/{types,parallel}.hpp) and link
+// liblsapgpu.so.  Each function mirrors its reference counterpart:
+//
+//   lsap::gpu::dgs_parallel              <- lsap::dgs_parallel              (parallel.hpp:80)
+//   lsap::gpu::evaluate_all_parallel     <- lsap::evaluate_all_parallel     (parallel.hpp:60-61)
+//   lsap::gpu::check_conflicts           <- lsap::check_conflicts           (parallel.hpp:65)
+//   lsap::gpu::apply_parallel_switches   <- lsap::apply_parallel_switches   (parallel.hpp:71-74)
+//
+// Same argument meaning, same results (bit for bit), same lsap::Error messages;
+// `workers` / `chunk` are validated and otherwise ignored (the reference's
+// results never depend on them, parallel.hpp:79-80).  A per-thread, per-device
+// context caches device memory and the CUDA graph between calls.
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "lsapgpu.h"
+
+namespace lsap::gpu {
+
+struct GpuConfig : ParallelConfig {
+  int device = 0;
+  bool use_graph = true;  // inner loop as one CUDA-graph launch per outer pass
+};
+
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    if (lsapgpu_create(&ctx_, device) != LSAPGPU_OK)
+      throw Error("lsapgpu: no usable sm_100 CUDA device " + std::to_string(device));
+  }
+  ~Context() { lsapgpu_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  lsapgpu_ctx* get() const { return ctx_; }
+
+  void check(int rc) const {
+    if (rc != LSAPGPU_OK) throw Error(lsapgpu_last_error(ctx_));
+  }
+
+  // Uploads the instance (validate, lossless narrowing, A and AT in HBM).
+  // Every call re-uploads: the functions below are pure like the reference's,
+  // so a caller that mutates or reallocates an Instance must never see a
+  // stale device copy.  Callers that solve one matrix repeatedly can keep a
+  // Context and call lsapgpu_set_matrix / lsapgpu_solve directly.
+  void set_instance(const Instance& inst) {
+    if (inst.n < 1) throw Error("instance size must be >= 1, got " + std::to_string(inst.n));
+    if (inst.benefits.size() != static_cast<std::size_t>(inst.n) * inst.n)
+      throw Error("benefit matrix is not " + std::to_string(inst.n) + "x" + std::to_string(inst.n));
+    check(lsapgpu_set_matrix(ctx_, inst.benefits.data(), inst.n, LSAPGPU_F64));
+  }
+
+ private:
+  lsapgpu_ctx* ctx_ = nullptr;
+};
+
+inline Context& context(int device) {
+  thread_local std::map<int, std::unique_ptr<Context>> ctxs;
+  auto& c = ctxs[device];
+  if (!c) c = std::make_unique<Context>(device);
+  return *c;
+}
+
+inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {}) {
+  inst.validate();
+  cfg.validate();
+  Context& ctx = context(cfg.device);
+  ctx.set_instance(inst);
+  lsapgpu_params p{};
+  p.seed = cfg.seed;
+  p.eps = cfg.improvement_epsilon;
+  p.reeval = cfg.reeval == ParallelConfig::Reeval::touched_only ? LSAPGPU_REEVAL_TOUCHED_ONLY
+                                                                 : LSAPGPU_REEVAL_TOUCHED_AND_CONFLICTED;
+  p.use_graph = cfg.use_graph ? 1 : 0;
+  p.deadline_ns = cfg.deadline ? static_cast<std::int64_t>(cfg.deadline->count()) : -1;
+  p.init_sigma = nullptr;
+  const std::int32_t n = inst.n;
+  SolveReport rep;
+  rep.assignment.sigma.resize(n);
+  rep.assignment.tau.resize(n);
+  lsapgpu_stats st{};
+  const std::int64_t cap = 100000 + 4096;
+  std::vector<std::int64_t> ts(cap);
+  std::vector<double> tv(cap);
+  std::int64_t tl = 0;
+  ctx.check(lsapgpu_solve(ctx.get(), &p, rep.assignment.sigma.data(), rep.assignment.tau.data(), &st,
+                          ts.data(), tv.data(), cap, &tl));
+  rep.assignment.value = st.value;
+  rep.outer_iterations = st.outer_iterations;
+  rep.switches_applied = st.switches_applied;
+  rep.terminated_by = st.terminated_by ? Termination::deadline : Termination::converged;
+  rep.elapsed = std::chrono::duration_cast<Duration>(std::chrono::duration<double, std::milli>(st.elapsed_ms));
+  const std::int64_t k = tl < cap ? tl : cap;
+  rep.objective_trace.reserve(static_cast<std::size_t>(k));
+  for (std::int64_t q = 0; q < k; ++q) rep.objective_trace.emplace_back(ts[q], tv[q]);
+  return rep;
+}
+
+inline void evaluate_all_parallel(const Instance& inst, const Assignment& asg, DeltaTables& tables,
+                                  const GpuConfig& cfg = {}) {
+  inst.validate();
+  cfg.validate();
+  if (asg.size() != inst.n) throw Error("assignment does not match instance");
+  Context& ctx = context(cfg.device);
+  ctx.set_instance(inst);
+  const std::int32_t n = inst.n;
+  std::vector<double> ad(n), jd(n);
+  std::vector<std::int32_t> ap(n), jp(n);
+  ctx.check(lsapgpu_evaluate_all(ctx.get(), asg.sigma.data(), cfg.improvement_epsilon, ad.data(), ap.data(),
+                                 jd.data(), jp.data()));
+  tables.agent_records.resize(n);
+  tables.job_records.resize(n);
+  for (std::int32_t k = 0; k < n; ++k) {
+    tables.agent_records[k] = {ap[k], ad[k], ap[k] >= 0};
+    tables.job_records[k] = {jp[k], jd[k], jp[k] >= 0};
+  }
+}
+
+inline ConflictSets check_conflicts(const DeltaTables& tables, const Assignment& asg, int device = 0) {
+  const std::int32_t n = asg.size();
+  if (tables.agent_records.size() != static_cast<std::size_t>(n) ||
+      tables.job_records.size() != static_cast<std::size_t>(n))
+    throw Error("delta tables do not match assignment size");
+  std::vector<double> ad(n), jd(n);
+  std::vector<std::int32_t> ap(n), jp(n);
+  for (std::int32_t k = 0; k < n; ++k) {  // parallel.cpp:166-173
+    ad[k] = tables.agent_records[k].active ? tables.agent_records[k].delta : 0.0;
+    ap[k] = tables.agent_records[k].partner;
+    jd[k] = tables.job_records[k].active ? tables.job_records[k].delta : 0.0;
+    jp[k] = tables.job_records[k].partner;
+  }
+  Context& ctx = context(device);
+  std::vector<std::uint8_t> res(n), con(n);
+  std::vector<std::int32_t> cj(n);
+  std::int32_t ncj = 0;
+  ConflictSets out;
+  out.agent_accepted.resize(n);
+  out.job_accepted.resize(n);
+  ctx.check(lsapgpu_check_conflicts(ctx.get(), n, ad.data(), ap.data(), jd.data(), jp.data(), asg.sigma.data(),
+                                    out.agent_accepted.data(), out.job_accepted.data(), res.data(), con.data(),
+                                    cj.data(), &ncj));
+  for (std::int32_t k = 0; k < n; ++k) {
+    if (res[k]) out.reserved.push_back(k);
+    if (con[k]) out.conflicted.push_back(k);
+  }
+  out.conflicted_jobs.assign(cj.begin(), cj.begin() + ncj);
+  return out;
+}
+
+inline std::pair<Assignment, std::vector<AppliedExchange>> apply_parallel_switches(
+    const Instance& inst, const Assignment& asg, const DeltaTables& tables, const ConflictSets& sets,
+    const GpuConfig& cfg = {}) {
+  inst.validate();
+  cfg.validate();
+  const std::int32_t n = inst.n;
+  if (asg.size() != n) throw Error("assignment does not match instance");
+  Context& ctx = context(cfg.device);
+  ctx.set_instance(inst);
+  std::vector<double> ad(n), jd(n);
+  std::vector<std::int32_t> ap(n), jp(n);
+  std::vector<std::uint8_t> aa(n), ja(n);
+  for (std::int32_t k = 0; k < n; ++k) {
+    ad[k] = tables.agent_records[k].delta;
+    ap[k] = tables.agent_records[k].partner;
+    aa[k] = tables.agent_records[k].active;
+    jd[k] = tables.job_records[k].delta;
+    jp[k] = tables.job_records[k].partner;
+    ja[k] = tables.job_records[k].active;
+  }
+  Assignment out = asg;
+  std::vector<std::int32_t> a1(n), a2(n), a3(n), a4(n);
+  std::vector<double> a5(n);
+  std::int32_t k = 0;
+  const int rc = lsapgpu_apply_parallel_switches(
+      ctx.get(), out.sigma.data(), out.tau.data(), &out.value, ad.data(), ap.data(), aa.data(), jd.data(),
+      jp.data(), ja.data(), sets.agent_accepted.data(), sets.job_accepted.data(), cfg.improvement_epsilon,
+      a1.data(), a2.data(), a3.data(), a4.data(), a5.data(), &k);
+  ctx.check(rc);
+  std::vector<AppliedExchange> applied(static_cast<std::size_t>(k));
+  for (std::int32_t q = 0; q < k; ++q) applied[q] = {a1[q], a2[q], a3[q], a4[q], a5[q]};
+  return {std::move(out), std::move(applied)};
+}
+
+}  // namespace lsap::gpu

@@ -263,7 +263,6 @@ class Context:
             raise Error(f"lsapgpu_create failed (rc={rc}): no usable sm_100 CUDA device {device}")
         self.h = h
         self.device = device
-        self._inst_key = None
 
     def close(self) -> None:
         if getattr(self, "h", None):
@@ -305,7 +304,6 @@ class Context:
             t = a.contiguous()
             nn = int(n if n is not None else t.shape[0])
             self._check(N.LIB.lsapgpu_set_matrix_device(self.h, t.data_ptr(), nn, dt))
-            self._inst_key = None
             return
         if hasattr(a, "numpy"):
             a = a.numpy()
@@ -319,25 +317,22 @@ class Context:
         if nn >= 1 and a.size != nn * nn:
             raise Error(f"benefit matrix is not {nn}x{nn}")
         self._check(N.LIB.lsapgpu_set_matrix(self.h, N.ptr(a), nn, dt))
-        self._inst_key = None
 
     def set_instance(self, inst: Instance) -> None:
-        key = (id(inst), inst.n, inst.benefits.ctypes.data)
-        if self._inst_key == key and self.n == inst.n:
-            return
+        """Upload an Instance (no caching: instances are plain mutable arrays,
+        so every reference-style call re-uploads; keep a Context and call
+        set_matrix once to amortise uploads over many solves)."""
         if inst.n < 1:
             raise Error(f"instance size must be >= 1, got {inst.n}")
         if inst.benefits.size != inst.n * inst.n:
             raise Error(f"benefit matrix is not {inst.n}x{inst.n}")
         self._check(N.LIB.lsapgpu_set_matrix(self.h, N.ptr(inst.benefits), inst.n, N.F64))
-        self._inst_key = key
 
     def generate(self, kind: str, n: int, seed: int = 0, param: Optional[float] = None) -> None:
         """On-device synthetic instance: int | f32 | unit | p2p | geom."""
         if param is None:
             param = {"int": 1000.0, "unit": 10.0, "geom": 100.0}.get(kind, 0.0)
         self._check(N.LIB.lsapgpu_generate(self.h, N.GEN[kind], n, seed & 0xFFFFFFFFFFFFFFFF, float(param)))
-        self._inst_key = None
 
     def read_rows(self, rows) -> np.ndarray:
         rows = np.ascontiguousarray(rows, np.int32)
@@ -408,7 +403,6 @@ class Context:
         self._check(N.LIB.lsapgpu_check_conflicts(self.h, n, N.ptr(ad), N.ptr(ap), N.ptr(jd), N.ptr(jp),
                                                   N.ptr(sigma), *[N.ptr(o) for o in outs], N.ptr(cj),
                                                   C.byref(k)))
-        self._inst_key = None  # vectors may have been resized
         return ConflictSets(reserved=np.flatnonzero(outs[2]).tolist(),
                             conflicted=np.flatnonzero(outs[3]).tolist(),
                             agent_accepted=outs[0], job_accepted=outs[1],
