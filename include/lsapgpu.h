@@ -125,6 +125,29 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
                   int32_t* tau_out, lsapgpu_stats* stats, int64_t* trace_switch,
                   double* trace_value, int64_t trace_cap, int64_t* trace_len);
 
+/* Multi-GPU solve, one process (and context) per GPU, every rank holding the
+ * full instance (SURVEY 8(e) placement (ii)).  Work items are owned by agent
+ * index (i % world == rank); after each scan the library calls `allgather`
+ * (enqueue on `stream`, e.g. ncclAllGather / torch.distributed over NVLink)
+ * to exchange `bytes_per_rank` bytes from send_dev into recv_dev
+ * (world * bytes_per_rank); the conflict check and apply then run replicated
+ * and deterministic, so every rank returns the same result, equal to
+ * lsapgpu_solve's.  world == 1 is lsapgpu_solve. */
+typedef int (*lsapgpu_allgather_fn)(void* user, const void* send_dev, void* recv_dev,
+                                    size_t bytes_per_rank, void* stream);
+typedef struct {
+  int32_t rank, world;
+  lsapgpu_allgather_fn allgather;
+  void* user;
+  void* send_dev; /* >= lsapgpu_dist_exchange_bytes(n, world) bytes, device memory */
+  void* recv_dev; /* world times that */
+} lsapgpu_dist;
+size_t lsapgpu_dist_exchange_bytes(int32_t n, int32_t world);
+int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsapgpu_dist* dist,
+                       int32_t* sigma_out, int32_t* tau_out, lsapgpu_stats* stats,
+                       int64_t* trace_switch, double* trace_value, int64_t trace_cap,
+                       int64_t* trace_len);
+
 /* lsap::evaluate_all_parallel: SoA records; partner -1 = inactive (delta 0). */
 int lsapgpu_evaluate_all(lsapgpu_ctx* ctx, const int32_t* sigma, double eps, double* agent_delta,
                          int32_t* agent_partner, double* job_delta, int32_t* job_partner);

@@ -25,7 +25,8 @@ EXPORTS = [
     "lsapgpu_last_error", "lsapgpu_stream", "lsapgpu_set_matrix", "lsapgpu_set_matrix_device",
     "lsapgpu_generate", "lsapgpu_n", "lsapgpu_storage", "lsapgpu_read_rows", "lsapgpu_solve",
     "lsapgpu_evaluate_all", "lsapgpu_check_conflicts", "lsapgpu_apply_parallel_switches",
-    "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
+    "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_solve_dist",
+    "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
 ]
 
 
@@ -62,6 +63,20 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class Dist(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("allgather", ALLGATHER_FN),
+        ("user", C.c_void_p),
+        ("send_dev", C.c_void_p),
+        ("recv_dev", C.c_void_p),
+    ]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -93,6 +108,9 @@ def _load() -> C.CDLL:
         "lsapgpu_random_perm": (None, [i32, u64, vp]),
         "lsapgpu_objective": (C.c_int, [vp, vp, C.POINTER(dbl)]),
         "lsapgpu_counters": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+        "lsapgpu_solve_dist": (C.c_int, [vp, C.POINTER(Params), C.POINTER(Dist), vp, vp, C.POINTER(Stats), vp, vp,
+                                         i64, C.POINTER(i64)]),
+        "lsapgpu_dist_exchange_bytes": (C.c_size_t, [i32, i32]),
         "lsapgpu_set_scan_timing": (C.c_int, [vp, C.c_int]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
                                           C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),

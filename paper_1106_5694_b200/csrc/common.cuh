@@ -87,6 +87,7 @@ struct Ctrl {
   int32_t iter;             // inner iterations so far in this solve (global stamp)
   uint32_t round;           // LFMM round counter (key epoch)
   int32_t work_count;       // items in the current work list
+  int32_t own_count;        // multi-GPU: items of this rank's share
   int32_t edge_count[2];    // ping-pong edge-list sizes
   int32_t inner_done;       // set when a commit found no active record
   int32_t expired;          // deadline hit

@@ -1,0 +1,116 @@
+// dist.cu -- record exchange for the multi-GPU solve (placement
+// (ii)): every rank holds a full replica of A / AT, scans only the work items
+// it owns (agent i with i % world == rank), packs the records it produced, and
+// after the caller's allgather (NCCL over NVLink) every rank merges all ranks'
+// records into its tables and rebuilds the proposal list.  The commit kernel
+// then runs replicated: its result does not depend on proposal order, so all
+// ranks apply identical batches and sigma never needs a broadcast.
+//
+// Exchange buffer per rank: 16-byte header {count} + count x Rec (32 B).
+#include "state.h"
+
+namespace lsapgpu {
+namespace {
+
+struct Rec {
+  int32_t agent, job;        // item (agent i, job tau[i]) at scan time
+  int32_t agent_partner, job_partner;
+  double agent_delta, job_delta;
+};
+static_assert(sizeof(Rec) == 32, "exchange record layout");
+
+// This rank's share of the work list (or of the identity list for a full sweep).
+__global__ void own_items_kernel(DevState st, int full, int32_t rank, int32_t world) {
+  const int32_t n = st.n;
+  const int32_t count = full ? n : st.ctrl->work_count;
+  for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+    const uint32_t w = full ? (static_cast<uint32_t>(k) | kItemAgent | kItemJob) : st.items[k];
+    const int32_t a = static_cast<int32_t>(w & kItemMask);
+    if (a % world != rank) continue;
+    const int pos = atomicAdd(&st.ctrl->own_count, 1);
+    st.items_own[pos] = w;
+  }
+}
+
+__global__ void reset_own_kernel(Ctrl* c) { c->own_count = 0; }
+
+__global__ void pack_kernel(DevState st, unsigned char* send) {
+  const int32_t count = st.ctrl->own_count;
+  Rec* out = reinterpret_cast<Rec*>(send + 16);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<long long*>(send) = count;
+  for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+    const uint32_t w = st.items_own[k];
+    const int32_t i = static_cast<int32_t>(w & kItemMask);
+    const int32_t j = st.tau[i];
+    Rec r;
+    r.agent = (w & kItemAgent) ? i : -1;
+    r.job = (w & kItemJob) ? j : -1;
+    r.agent_partner = st.agent_partner[i];
+    r.agent_delta = st.agent_delta[i];
+    r.job_partner = st.job_partner[j];
+    r.job_delta = st.job_delta[j];
+    // holder of the job is i (the item's agent): carried in agent when the
+    // agent record is not part of the item
+    if (r.agent < 0) r.agent = -2 - i;
+    out[k] = r;
+  }
+}
+
+// Write every rank's records and append the active ones as proposals
+// {slot, proposer, partner, job} (the layout the pair scan emits).
+__global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t world, size_t bytes_per_rank) {
+  const int32_t n = st.n;
+  const int P = st.ctrl->parity;
+  for (int32_t r = 0; r < world; ++r) {
+    const unsigned char* base = recv + static_cast<size_t>(r) * bytes_per_rank;
+    const int32_t count = static_cast<int32_t>(*reinterpret_cast<const long long*>(base));
+    const Rec* in = reinterpret_cast<const Rec*>(base + 16);
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+      const Rec rec = in[k];
+      const bool has_agent = rec.agent >= 0;
+      const int32_t i = has_agent ? rec.agent : -2 - rec.agent;
+      if (has_agent) {
+        st.agent_delta[i] = rec.agent_delta;
+        st.agent_partner[i] = rec.agent_partner;
+        if (rec.agent_partner >= 0) {
+          const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
+          st.edges[P][pos] = make_int4(i, i, rec.agent_partner, rec.job >= 0 ? rec.job : st.tau[i]);
+        }
+      }
+      if (rec.job >= 0) {
+        st.job_delta[rec.job] = rec.job_delta;
+        st.job_partner[rec.job] = rec.job_partner;
+        if (rec.job_partner >= 0) {
+          const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
+          st.edges[P][pos] = make_int4(n + rec.job, i, rec.job_partner, rec.job);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t dist_exchange_bytes(int32_t n, int32_t world) {
+  const size_t per = (static_cast<size_t>(n) + world - 1) / world;
+  return ((16 + per * sizeof(Rec)) + 255) / 256 * 256;
+}
+
+cudaError_t launch_dist_own_items(const DevState& d, int full, int32_t rank, int32_t world, cudaStream_t st) {
+  reset_own_kernel<<<1, 1, 0, st>>>(d.ctrl);
+  own_items_kernel<<<148, 256, 0, st>>>(d, full, rank, world);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dist_pack(const DevState& d, void* send, cudaStream_t st) {
+  pack_kernel<<<148, 256, 0, st>>>(d, static_cast<unsigned char*>(send));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dist_merge(const DevState& d, const void* recv, int32_t world, size_t bytes_per_rank,
+                              cudaStream_t st) {
+  merge_kernel<<<148, 256, 0, st>>>(d, static_cast<const unsigned char*>(recv), world, bytes_per_rank);
+  return cudaGetLastError();
+}
+
+}  // namespace lsapgpu

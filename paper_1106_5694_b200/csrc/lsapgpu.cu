@@ -186,6 +186,7 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.conf_stamp, N, true));
   CK(valloc(ctx, &d.rej_stamp, N2, true));
   CK(valloc(ctx, &d.items, N, false));
+  CK(valloc(ctx, &d.items_own, N, false));
   d.log_cap = std::max<int64_t>(1 << 20, 8 * static_cast<int64_t>(n));
   CK(valloc(ctx, &d.log, static_cast<size_t>(d.log_cap), false));
   d.part_cap = (static_cast<int64_t>(n) + 8) * 16;
@@ -742,9 +743,20 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
   return LSAPGPU_OK;
 }
 
+size_t lsapgpu_dist_exchange_bytes(int32_t n, int32_t world) {
+  return world < 1 || n < 1 ? 0 : dist_exchange_bytes(n, world);
+}
+
 int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma_out,
                   int32_t* tau_out, lsapgpu_stats* stats, int64_t* trace_switch, double* trace_value,
                   int64_t trace_cap, int64_t* trace_len) {
+  return lsapgpu_solve_dist(ctx, params, nullptr, sigma_out, tau_out, stats, trace_switch, trace_value,
+                            trace_cap, trace_len);
+}
+
+int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsapgpu_dist* dist,
+                       int32_t* sigma_out, int32_t* tau_out, lsapgpu_stats* stats, int64_t* trace_switch,
+                       double* trace_value, int64_t trace_cap, int64_t* trace_len) {
   if (!ctx) return LSAPGPU_ERR_INVALID;
   if (!ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
   if (!params || !sigma_out) return fail(ctx, LSAPGPU_ERR_INVALID, "null argument");
@@ -755,6 +767,29 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   if (P.reeval != 0 && P.reeval != 1) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown reeval policy");
   const int32_t n = ctx->n_matrix;
   DevState& d = ctx->d;
+  const bool multi = dist && dist->world > 1;
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world))
+    return fail(ctx, LSAPGPU_ERR_INVALID, "invalid rank / world");
+  if (multi && (!dist->allgather || !dist->send_dev || !dist->recv_dev))
+    return fail(ctx, LSAPGPU_ERR_INVALID, "multi-GPU solve needs an allgather callback and exchange buffers");
+  const size_t xbytes = multi ? dist_exchange_bytes(n, dist->world) : 0;
+  // one distributed step: this rank's items -> scan -> pack -> allgather -> merge
+  auto dist_round = [&](int full) -> int {
+    CK(launch_dist_own_items(d, full, dist->rank, dist->world, ctx->stream));
+    ctx->launches += 2;
+    DevState ds = d;
+    ds.use_own = 1;
+    ds.emit_edges = 0;
+    CK(launch_scan(ds, ctx->scan_plan, 0, ctx->stream));
+    ++ctx->launches;
+    CK(launch_dist_pack(d, dist->send_dev, ctx->stream));
+    ++ctx->launches;
+    if (dist->allgather(dist->user, dist->send_dev, dist->recv_dev, xbytes, ctx->stream) != 0)
+      return fail(ctx, LSAPGPU_ERR_CUDA, "allgather callback failed");
+    CK(launch_dist_merge(d, dist->recv_dev, dist->world, xbytes, ctx->stream));
+    ++ctx->launches;
+    return LSAPGPU_OK;
+  };
 
   std::vector<int32_t> sigma0(n);
   if (P.init_sigma) {
@@ -789,7 +824,7 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
         ctx->ctrl_dev, P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns()));
     ++ctx->launches;
     CK(cudaGetLastError());
-    if (P.use_graph && (!ctx->exec || ctx->graph_eps != d.eps || ctx->graph_policy != d.policy)) {
+    if (P.use_graph && !multi && (!ctx->exec || ctx->graph_eps != d.eps || ctx->graph_policy != d.policy)) {
       rc = build_graph(ctx);
       if (rc) return rc;
     }
@@ -811,14 +846,30 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
     begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
     ++ctx->launches;
     CK(cudaGetLastError());
-    rc = run_scan(ctx, 1);
+    if (multi) {
+      rc = dist_round(1);
+    } else {
+      rc = run_scan(ctx, 1);
+    }
     if (rc) return rc;
     ++launches;
     S.pair_items += n;
     S.agent_scans += n;
     S.job_scans += n;
     for (;;) {  // inner loop; repeats only to drain a full delta log
-      if (P.use_graph) {
+      if (multi) {
+        for (;;) {
+          CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
+          ++ctx->launches;
+          rc = pull_ctrl(ctx);
+          if (rc) return rc;
+          const Ctrl& C = *ctx->ctrl_host;
+          if (C.inner_done || C.expired || C.drain || C.error) break;
+          rc = dist_round(0);
+          if (rc) return rc;
+          ++launches;
+        }
+      } else if (P.use_graph) {
         CK(cudaGraphLaunch(ctx->exec, ctx->stream));
         ++graph_launches;
         rc = pull_ctrl(ctx);
@@ -893,10 +944,11 @@ int lsapgpu_solve(lsapgpu_ctx* ctx, const lsapgpu_params* params, int32_t* sigma
   S.job_scans += C.job_scans - base.job_scans;
   S.lfmm_rounds = C.lfmm_rounds - base.lfmm_rounds;
   S.switches_applied = switches;
-  S.scan_launches = P.use_graph ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
+  const bool graphed = P.use_graph && !multi;
+  S.scan_launches = graphed ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
   // every body pass of the graph is one commit + one scan launch; the last
   // pass per graph launch finds no active record and exits early
-  if (P.use_graph) ctx->launches += 2 * (S.inner_iterations + graph_launches);
+  if (graphed) ctx->launches += 2 * (S.inner_iterations + graph_launches);
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 

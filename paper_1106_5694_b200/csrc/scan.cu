@@ -304,8 +304,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 
-  const int32_t count = full ? n : st.ctrl->work_count;
+  const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
   if (count <= 0) return;
+  const uint32_t* __restrict__ items = st.use_own ? st.items_own : st.items;
   const int32_t groups = (count + M - 1) / M;
   // Segments: split an item group over several CTAs when the list is short,
   // picking the split that best fills whole waves of the persistent grid.
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
       it.flags = 0;
       return it;
     }
-    const uint32_t w = full ? (static_cast<uint32_t>(idx) | kItemAgent | kItemJob) : st.items[idx];
+    const uint32_t w = full ? (static_cast<uint32_t>(idx) | kItemAgent | kItemJob) : items[idx];
     it.agent = static_cast<int32_t>(w & kItemMask);
     it.job = tau[it.agent];
     it.flags = w & (kItemAgent | kItemJob);
@@ -533,13 +534,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
                 if (im.flags & kItemAgent) {
                   st.agent_delta[im.agent] = active ? d : 0.0;
                   st.agent_partner[im.agent] = active ? k : -1;
-                  emit = active;
+                  emit = active && st.emit_edges;
                   entry = make_int4(im.agent, im.agent, k, im.job);
                 }
               } else if (im.flags & kItemJob) {
                 st.job_delta[im.job] = active ? d : 0.0;
                 st.job_partner[im.job] = active ? k : -1;
-                emit = active;
+                emit = active && st.emit_edges;
                 entry = make_int4(n + im.job, im.agent, k, im.job);
               }
             }

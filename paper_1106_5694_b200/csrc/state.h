@@ -62,6 +62,12 @@ struct DevState {
   Ctrl* ctrl = nullptr;
   double eps = 0.0;
   int policy = 0;  // 0 touched_and_conflicted, 1 touched_only
+
+  // multi-GPU (dist.cu): this rank's share of the work list, and whether the
+  // scan appends proposals itself (single GPU) or the record merge does
+  uint32_t* items_own = nullptr;
+  int use_own = 0;
+  int emit_edges = 1;
 };
 
 // ---- launchers (implemented in the .cu files) -------------------------------
@@ -101,6 +107,13 @@ struct ScanPlan {
 ScanPlan plan_scan(const DevState& d, int num_sms);
 // full sweep (identity work list, count n) when full != 0, else the device work list
 cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+
+// dist.cu (multi-GPU record exchange)
+size_t dist_exchange_bytes(int32_t n, int32_t world);
+cudaError_t launch_dist_own_items(const DevState& d, int full, int32_t rank, int32_t world, cudaStream_t st);
+cudaError_t launch_dist_pack(const DevState& d, void* send, cudaStream_t st);
+cudaError_t launch_dist_merge(const DevState& d, const void* recv, int32_t world, size_t bytes_per_rank,
+                              cudaStream_t st);
 
 // commit.cu
 enum CommitMode : int { kCommitSolve = 0, kCommitCheckOnly = 1, kCommitApplyOnly = 2 };

@@ -341,7 +341,10 @@ class Context:
         return out
 
     # -- solver -----------------------------------------------------------
-    def solve(self, cfg: ParallelConfig = ParallelConfig(), init_sigma=None, trace: bool = True):
+    def solve(self, cfg: ParallelConfig = ParallelConfig(), init_sigma=None, trace: bool = True,
+              dist=None):
+        """lsap::dgs_parallel on this context's matrix.  ``dist`` (see
+        paper_1106_5694_b200.dist) makes it one rank of a multi-GPU solve."""
         cfg.validate()
         n = self.n
         p = N.Params()
@@ -360,9 +363,15 @@ class Context:
         ts = np.empty(max(cap, 1), np.int64)
         tv = np.empty(max(cap, 1))
         tl = C.c_int64(0)
-        self._check(N.LIB.lsapgpu_solve(self.h, C.byref(p), N.ptr(sigma), N.ptr(tau), C.byref(st),
-                                        N.ptr(ts) if trace else None, N.ptr(tv) if trace else None,
-                                        cap, C.byref(tl)))
+        if dist is None:
+            rc = N.LIB.lsapgpu_solve(self.h, C.byref(p), N.ptr(sigma), N.ptr(tau), C.byref(st),
+                                     N.ptr(ts) if trace else None, N.ptr(tv) if trace else None, cap, C.byref(tl))
+        else:
+            rc = N.LIB.lsapgpu_solve_dist(self.h, C.byref(p), C.byref(dist.struct(self)), N.ptr(sigma),
+                                          N.ptr(tau), C.byref(st), N.ptr(ts) if trace else None,
+                                          N.ptr(tv) if trace else None, cap, C.byref(tl))
+            dist.raise_pending()
+        self._check(rc)
         k = min(tl.value, cap)
         rep = SolveReport(
             assignment=Assignment(sigma, tau, st.value),
