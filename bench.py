@@ -202,19 +202,18 @@ def run_ours(args, wl) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_1106_5694_b200 as g
-    from oracle.oracle import Oracle
 
     kind, n, iseed, param, desc = wl
     # replicas: every rank solves its own instance (seed offset by rank); see DESIGN.md "Multi-GPU"
     iseed = iseed + rank
-    orc = Oracle()
     ctx = g.Context(local)
     cfg = g.ParallelConfig(seed=0)
     stream = torch.cuda.ExternalStream(ctx.stream)
 
-    # the input instance (fp64, like lsap::Instance), generated by the oracle recipe
+    # the input instance (fp64 host matrix, like lsap::Instance), built by the
+    # package's on-device generator (same recipe and bits as the reference's)
     if n <= 30000:
-        a_host = torch.from_numpy(orc.generate(kind, n, iseed, param)).pin_memory()
+        a_host = torch.from_numpy(g.generate_instance(kind, n, iseed, param, device=local)).pin_memory()
     else:
         ctx.generate(kind, n, iseed, param)  # too big for a host fp64 copy; build on device
         a_host = None

@@ -22,6 +22,7 @@ from .lsap import (  # noqa: F401
     context,
     dgs_parallel,
     evaluate_all_parallel,
+    generate_instance,
     initial_random,
     is_permutation,
     make_assignment,

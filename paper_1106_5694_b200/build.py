@@ -52,6 +52,10 @@ def up_to_date() -> bool:
 
 def _compile(src: str) -> tuple:
     obj = os.path.join(OBJ_DIR, os.path.basename(src).replace(".cu", ".o"))
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+        [os.path.join(ROOT, "include", "lsapgpu.h")]
+    if os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in [src, *headers]):
+        return src, obj, 0, open(obj + ".ptxas.txt").read() if os.path.exists(obj + ".ptxas.txt") else ""
     cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, r.returncode, r.stdout + r.stderr

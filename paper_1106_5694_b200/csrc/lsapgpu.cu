@@ -12,8 +12,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/lsapgpu.h"
@@ -64,6 +68,73 @@ struct Buf {
   size_t bytes = 0;
 };
 
+constexpr size_t kUploadChunk = 64ull << 20;  // rows per H2D chunk: ~64 MB of source
+constexpr int kRing = 3;                       // pinned bounce buffers (pageable sources)
+constexpr size_t kStageKeep = 16ull << 30;     // keep the device staging copy up to this size
+
+int upload_threads() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return static_cast<int>(std::max(2u, std::min(8u, hw ? hw / 2 : 2u)));
+}
+
+// Fixed pool of host threads for the pageable -> pinned copies: run(fn) calls
+// fn(t) for t = 0..size()-1, t = 0 on the calling thread, and returns when all
+// are done.
+class HostPool {
+ public:
+  explicit HostPool(int n) : n_(n) {
+    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  void run(const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> l(m_);
+    done_cv_.wait(l, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f = nullptr;
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        f = fn_;
+      }
+      (*f)(t);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 struct lsapgpu_ctx {
@@ -98,6 +169,17 @@ struct lsapgpu_ctx {
 
   // cumulative transfer / launch counters (bench.py's e2e and gpu_launches)
   int64_t h2d = 0, d2h = 0, launches = 0;
+
+  // host upload pipeline (lsapgpu_set_matrix)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr;
+  cudaEvent_t ev_chunk[kRing] = {};
+  Buf stage;                      // device copy of the source matrix
+  uint32_t* chunk_flags = nullptr;
+  int chunk_flags_cap = 0;
+  void* ring[kRing] = {};         // pinned bounce buffers
+  size_t ring_bytes = 0;
+  HostPool* pool = nullptr;
 };
 
 namespace {
@@ -111,7 +193,7 @@ cudaError_t cpy(lsapgpu_ctx* ctx, void* dst, const void* src, size_t bytes, cuda
                 cudaStream_t st) {
   if (kind == cudaMemcpyHostToDevice) ctx->h2d += static_cast<int64_t>(bytes);
   if (kind == cudaMemcpyDeviceToHost) ctx->d2h += static_cast<int64_t>(bytes);
-  return cudaMemcpyAsync(dst, src, bytes, kind, st);
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);  // UVA: any host/device pointer
 }
 
 #define CK(expr)                                                                         \
@@ -215,26 +297,15 @@ int push_ctrl(lsapgpu_ctx* ctx) {
   return LSAPGPU_OK;
 }
 
-// Builds A/AT from a layout source; src_rows_dev is a device pointer for memory sources.
-int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
-  int rc = ensure_vectors(ctx, n);
-  if (rc) return rc;
-  ctx->n_matrix = 0;
-  drop_graph(ctx);
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(uint32_t), ctx->stream));
-  CK(launch_classify(src, n, 0, n, ctx->flags_dev, ctx->stream));
-  ++ctx->launches;
-  uint32_t flags = 0;
-  CK(cpy(ctx, &flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
-  int storage = kF64;
-  if (!(flags & 2u))
-    storage = kI16;
-  else if (!(flags & 4u))
-    storage = kI32;
-  else if (!(flags & 8u))
-    storage = kF32;
+int storage_of_flags(uint32_t flags) {
+  if (!(flags & 2u)) return kI16;
+  if (!(flags & 4u)) return kI32;
+  if (!(flags & 8u)) return kF32;
+  return kF64;
+}
+
+// (Re)points A/AT at an allocation large enough for n x ld elements of `storage`.
+int alloc_matrix(lsapgpu_ctx* ctx, int32_t n, int storage) {
   const int64_t ld = pitch_of(n);
   const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(ld) * esize(storage);
   if (ctx->mat.bytes < 2 * bytes) {
@@ -248,13 +319,162 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   d.storage = storage;
   d.A = ctx->mat.p;
   d.AT = static_cast<unsigned char*>(ctx->mat.p) + bytes;
-  CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), ld,
+  return LSAPGPU_OK;
+}
+
+void finish_matrix(lsapgpu_ctx* ctx, int32_t n) {
+  ctx->scan_plan = plan_scan(ctx->d, ctx->num_sms);
+  ctx->commit_plan = plan_commit(ctx->d);
+  ctx->n_matrix = n;
+}
+
+// Builds A/AT from a layout source; src_rows_dev is a device pointer for memory sources.
+int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
+  int rc = ensure_vectors(ctx, n);
+  if (rc) return rc;
+  ctx->n_matrix = 0;
+  drop_graph(ctx);
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(uint32_t), ctx->stream));
+  CK(launch_classify(src, n, 0, n, ctx->flags_dev, ctx->stream));
+  ++ctx->launches;
+  uint32_t flags = 0;
+  CK(cpy(ctx, &flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+  const int storage = storage_of_flags(flags);
+  if ((rc = alloc_matrix(ctx, n, storage))) return rc;
+  DevState& d = ctx->d;
+  CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
                          ctx->stream));
   ++ctx->launches;
   CK(cudaStreamSynchronize(ctx->stream));
-  ctx->scan_plan = plan_scan(d, ctx->num_sms);
-  ctx->commit_plan = plan_commit(d);
-  ctx->n_matrix = n;
+  finish_matrix(ctx, n);
+  return LSAPGPU_OK;
+}
+
+// Host upload (lsapgpu_set_matrix): the matrix crosses PCIe in row chunks
+// into a device staging copy while the compute stream classifies each chunk
+// (Instance::validate + narrowest-storage choice) and builds its rows of A
+// and columns of AT.  The storage type is speculated from chunk 0; if a later
+// chunk needs a wider type, the whole layout is rebuilt from the staging copy
+// once the last chunk is in (only inputs whose first rows are narrower than
+// the rest pay for that).  Pageable host memory is first copied into a ring
+// of pinned buffers by a pool of host threads, so it streams at close to the
+// pinned PCIe rate instead of the driver's single-threaded pageable path.
+int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
+  int rc = ensure_vectors(ctx, n);
+  if (rc) return rc;
+  ctx->n_matrix = 0;
+  drop_graph(ctx);
+  const size_t es = src_size(dtype);
+  const size_t row_bytes = static_cast<size_t>(n) * es;
+  const size_t total = row_bytes * static_cast<size_t>(n);
+  // staging copy of the source matrix (kept for reuse up to 16 GB)
+  if (ctx->stage.bytes < total) {
+    if (ctx->stage.p) cudaFree(ctx->stage.p);
+    ctx->stage.p = nullptr;
+    ctx->stage.bytes = 0;
+    CK(cudaMalloc(&ctx->stage.p, total));
+    ctx->stage.bytes = total;
+  }
+  int64_t chunk_rows = static_cast<int64_t>(kUploadChunk / row_bytes) / 32 * 32;
+  if (chunk_rows < 32) chunk_rows = 32;
+  if (chunk_rows > n) chunk_rows = n;
+  const int nchunks = static_cast<int>((n + chunk_rows - 1) / chunk_rows);
+  if (static_cast<int>(ctx->chunk_flags_cap) < nchunks) {
+    if (ctx->chunk_flags) cudaFree(ctx->chunk_flags);
+    ctx->chunk_flags = nullptr;
+    ctx->chunk_flags_cap = 0;
+    CK(cudaMalloc(&ctx->chunk_flags, sizeof(uint32_t) * nchunks));
+    ctx->chunk_flags_cap = nchunks;
+  }
+  CK(cudaMemsetAsync(ctx->chunk_flags, 0, sizeof(uint32_t) * nchunks, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_ready, 0));
+
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, data) == cudaSuccess &&
+                      (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeDevice ||
+                       attr.type == cudaMemoryTypeManaged);
+  cudaGetLastError();
+  const size_t ring_bytes = static_cast<size_t>(chunk_rows) * row_bytes;
+  if (!pinned && ctx->ring_bytes < ring_bytes) {
+    for (auto& r : ctx->ring)
+      if (r) cudaFreeHost(r);
+    for (auto& r : ctx->ring) r = nullptr;
+    ctx->ring_bytes = 0;
+    for (auto& r : ctx->ring) CK(cudaMallocHost(&r, ring_bytes));
+    ctx->ring_bytes = ring_bytes;
+  }
+  if (!pinned && !ctx->pool) ctx->pool = new HostPool(upload_threads());
+
+  int storage = -1;
+  LayoutSource src;
+  src.kind = 0;
+  src.src = ctx->stage.p;
+  src.src_dtype = dtype;
+  for (int k = 0; k < nchunks; ++k) {
+    const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
+    const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
+    const size_t off = static_cast<size_t>(r0) * row_bytes, len = static_cast<size_t>(rows) * row_bytes;
+    unsigned char* dst = static_cast<unsigned char*>(ctx->stage.p) + off;
+    const unsigned char* hsrc = static_cast<const unsigned char*>(data) + off;
+    cudaEvent_t done = ctx->ev_chunk[k % kRing];
+    if (pinned) {
+      CK(cpy(ctx, dst, hsrc, len, cudaMemcpyHostToDevice, ctx->copy_stream));
+    } else {
+      const int b = k % kRing;
+      if (k >= kRing) CK(cudaEventSynchronize(ctx->ev_chunk[b]));  // ring slot's previous DMA done
+      unsigned char* pin = static_cast<unsigned char*>(ctx->ring[b]);
+      const int T = ctx->pool->size();
+      ctx->pool->run([&](int t) {
+        const size_t a = len * t / T, e = len * (t + 1) / T;
+        std::memcpy(pin + a, hsrc + a, e - a);
+      });
+      CK(cpy(ctx, dst, pin, len, cudaMemcpyHostToDevice, ctx->copy_stream));
+    }
+    CK(cudaEventRecord(done, ctx->copy_stream));
+    CK(cudaStreamWaitEvent(ctx->stream, done, 0));
+    CK(launch_classify(src, n, r0, rows, ctx->chunk_flags + k, ctx->stream));
+    ++ctx->launches;
+    if (k == 0) {  // speculate the storage from the first chunk
+      uint32_t f0 = 0;
+      CK(cpy(ctx, &f0, ctx->chunk_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (f0 & 1u) {
+        CK(cudaStreamSynchronize(ctx->copy_stream));
+        return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+      }
+      storage = storage_of_flags(f0);
+      if ((rc = alloc_matrix(ctx, n, storage))) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        return rc;
+      }
+    }
+    CK(launch_build_layout(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
+                           const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->stream));
+    ++ctx->launches;
+  }
+  std::vector<uint32_t> fl(nchunks);
+  CK(cpy(ctx, fl.data(), ctx->chunk_flags, sizeof(uint32_t) * nchunks, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  uint32_t all = 0;
+  for (uint32_t f : fl) all |= f;
+  if (all & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+  const int final_storage = storage_of_flags(all);
+  if (final_storage != storage) {  // a later chunk needs a wider type: rebuild everything
+    if ((rc = alloc_matrix(ctx, n, final_storage))) return rc;
+    CK(launch_build_layout(src, n, 0, n, final_storage, const_cast<void*>(ctx->d.A),
+                           const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->stream));
+    ++ctx->launches;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  if (total > kStageKeep) {
+    cudaFree(ctx->stage.p);
+    ctx->stage.p = nullptr;
+    ctx->stage.bytes = 0;
+  }
+  finish_matrix(ctx, n);
   return LSAPGPU_OK;
 }
 
@@ -398,9 +618,17 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||
       cudaMalloc(&ctx->flags_dev, sizeof(uint32_t)) != cudaSuccess ||
-      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming) != cudaSuccess) {
     lsapgpu_destroy(ctx);
     return LSAPGPU_ERR_CUDA;
+  }
+  for (auto& e : ctx->ev_chunk) {
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      lsapgpu_destroy(ctx);
+      return LSAPGPU_ERR_CUDA;
+    }
   }
   std::memset(ctx->ctrl_host, 0, sizeof(Ctrl));
   ctx->ctrl_host->round = 1;
@@ -421,6 +649,16 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   if (ctx->flags_dev) cudaFree(ctx->flags_dev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+  if (ctx->stage.p) cudaFree(ctx->stage.p);
+  if (ctx->chunk_flags) cudaFree(ctx->chunk_flags);
+  for (auto& r : ctx->ring)
+    if (r) cudaFreeHost(r);
+  delete ctx->pool;
+  for (auto& e : ctx->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -450,18 +688,9 @@ int lsapgpu_set_matrix(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dt
   CK(cudaSetDevice(ctx->device));
   if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
   if (dtype < 0 || dtype > 3) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown matrix dtype");
-  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(n) * src_size(dtype);
-  void* stage = nullptr;
-  CK(cudaMalloc(&stage, bytes));
-  cudaError_t e = cpy(ctx, stage, data, bytes, cudaMemcpyHostToDevice, ctx->stream);
-  if (e != cudaSuccess) {
-    cudaFree(stage);
-    return fail(ctx, LSAPGPU_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
-  }
-  const int rc = lsapgpu_set_matrix_device(ctx, stage, n, dtype);
-  cudaStreamSynchronize(ctx->stream);
-  cudaFree(stage);
-  return rc;
+  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  if (!data) return fail(ctx, LSAPGPU_ERR_INVALID, "null benefit matrix");
+  return upload_host(ctx, data, n, dtype);
 }
 
 int lsapgpu_generate(lsapgpu_ctx* ctx, int32_t kind, int32_t n, uint64_t seed, double param) {

@@ -1,0 +1,506 @@
+// scan_resident.cuh -- the pair scan with every operand in shared memory.
+//
+// Same work item and arithmetic as the streaming kernel (scan_kernel.cuh):
+// item = agent i with its job j0 = tau[i]; one pass over i' = 0..n-1 with
+// t = tau[i'], x = AT[j0][i'], g = A[i][t], c = acur[i'] yields agent i's
+// record (candidate (g - s) + (x - c), tie index t) and job j0's record
+// (candidate (x - s) + (g - c), tie index i') -- the reference's
+// exchange_scan pair (kernels_scalar.cpp:6-25, solver_state.hpp:78-92).
+//
+// Layout for n small enough that the frozen per-scan state fits on chip
+// (C3: n = 10000, int16): tau (as uint16) and acur stay resident in shared
+// memory for the whole launch, and BOTH rows of an item, A[i,:] and
+// AT[j0,:], arrive by TMA bulk copies into a double-buffered stage.  A
+// dedicated producer warp (warp 15) prefetches the next stage's item
+// metadata in registers and issues the copies as soon as the consumers
+// release a buffer; the 15 consumer warps never touch global memory in the
+// inner loop, so the HBM stream is limited only by the TMA queue depth
+// (two stages = 4 rows in flight per SM) and not by register-held loads.
+//
+// Algorithmic HBM bytes: 2 * n * sizeof(elem) per item (the two rows).
+#pragma once
+
+#include "scan_kernel.cuh"
+
+namespace lsapgpu {
+namespace scan_detail {
+
+constexpr int kResThreads = 512;            // 15 consumer warps + 1 producer warp
+constexpr int kResWarps = kResThreads / 32 - 1;
+constexpr int kResEdgeBuf = 256;
+
+struct ResInfo {
+  int32_t agent;  // -1: no item in this slot (tail group)
+  int32_t job;    // tau[agent]
+  uint32_t flags;
+  int32_t pad;
+  double sv;      // acur[agent], widened (exact for every storage type)
+};
+
+template <class E>
+__device__ __forceinline__ void lds_tau(const uint16_t* p, int32_t (&t)[16 / sizeof(E)]) {
+  constexpr int V = 16 / sizeof(E);
+  if constexpr (V == 8) {
+    const uint4 w = *reinterpret_cast<const uint4*>(p);
+    const uint32_t a[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      t[2 * k] = static_cast<int32_t>(a[k] & 0xFFFFu);
+      t[2 * k + 1] = static_cast<int32_t>(a[k] >> 16);
+    }
+  } else if constexpr (V == 4) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+    t[0] = static_cast<int32_t>(w.x & 0xFFFFu);
+    t[1] = static_cast<int32_t>(w.x >> 16);
+    t[2] = static_cast<int32_t>(w.y & 0xFFFFu);
+    t[3] = static_cast<int32_t>(w.y >> 16);
+  } else {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+    t[0] = static_cast<int32_t>(w & 0xFFFFu);
+    t[1] = static_cast<int32_t>(w >> 16);
+  }
+}
+
+// Packed-32 fast body (int16 storage, n <= 16384): the item-independent part
+// of the key, s, is left out of the running maxima and subtracted from the
+// winner at finalisation (d' = g + x - c lies in [-98301, 98301], so
+// d' + 2^17 fits the 18-bit field and the unsigned order is unchanged).
+//   agent key = (d' + 2^17) * 2^14 + (16383 - t)
+//   job   key = (d' + 2^17) * 2^14 + (16383 - i')
+constexpr uint32_t kResKey = (static_cast<uint32_t>(1u << 17) << 14) + 16383u;
+
+template <int M>
+__device__ __forceinline__ void res_step_p32(const uint4& tw, const uint4& cw, const uint4 (&xw)[M],
+                                             int32_t i0, const char* __restrict__ rowsA_b,
+                                             uint32_t pitch_b, uint32_t (&ka)[M], uint32_t (&kj)[M]) {
+  const uint32_t tws[4] = {tw.x, tw.y, tw.z, tw.w};
+  const uint32_t cws[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const uint32_t word_t = tws[h >> 1], word_c = cws[h >> 1];
+    const uint32_t t = (h & 1) ? (word_t >> 16) : (word_t & 0xFFFFu);
+    // c * 2^14, sign-extended from the 16-bit half
+    const int32_t c14 = (h & 1) ? (static_cast<int32_t>(word_c & 0xFFFF0000u) >> 2)
+                                : (static_cast<int32_t>(word_c << 16) >> 2);
+    const uint32_t pa = kResKey - static_cast<uint32_t>(c14) - t;
+    const uint32_t pj = (kResKey - static_cast<uint32_t>(h)) - static_cast<uint32_t>(c14) -
+                        static_cast<uint32_t>(i0);
+    const char* gp = rowsA_b + 2 * t;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int32_t g = *reinterpret_cast<const int16_t*>(gp + m * pitch_b);
+      const uint32_t xword = (&xw[m].x)[h >> 1];
+      const int32_t x = (h & 1) ? (static_cast<int32_t>(xword) >> 16)
+                                : static_cast<int32_t>(static_cast<int16_t>(xword & 0xFFFFu));
+      const uint32_t f = static_cast<uint32_t>(g + x);
+      ka[m] = max(ka[m], f * 16384u + pa);
+      kj[m] = max(kj[m], f * 16384u + pj);
+    }
+  }
+}
+
+// mbarrier wait that suspends the warp between polls instead of spinning
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LAB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra LAB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+
+// smem: tau16[ld] | acur[ld] | stages [bufs][2][M][ld] (A rows, AT rows) |
+//       full[4], empty[4], res[1] mbarriers | red[bufs][NW][2M]
+template <class E, int M, int KM>
+__global__ void __launch_bounds__(kResThreads, 1)
+    pair_scan_res_kernel(DevState st, int full, int bufs, int max_segments) {
+  using Acc = typename Traits<E>::Acc;
+  constexpr int V = 16 / sizeof(E);
+  constexpr int NW = kResWarps;
+  constexpr int32_t kBlk = 32 * V;
+  constexpr int32_t kStride = NW * kBlk;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int32_t n = st.n;
+  const int64_t ld = st.ld;
+  const E* __restrict__ A = static_cast<const E*>(st.A);
+  const E* __restrict__ AT = static_cast<const E*>(st.AT);
+  const E* __restrict__ acur_g = static_cast<const E*>(st.acur);
+  const int32_t* __restrict__ tau_g = st.tau;
+
+  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(E);
+  uint16_t* tau_s = reinterpret_cast<uint16_t*>(smem_raw);
+  E* acur_s = reinterpret_cast<E*>(smem_raw + ((static_cast<size_t>(ld) * 2 + 127) / 128) * 128);
+  unsigned char* stage_base = reinterpret_cast<unsigned char*>(acur_s) + ((row_bytes + 127) / 128) * 128;
+  const size_t stage_bytes = 2 * M * row_bytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stage_base + bufs * stage_bytes);
+  uint64_t* empty_bar = full_bar + kMaxBufs;
+  uint64_t* res_bar = full_bar + 2 * kMaxBufs;
+  Track<KM>* red = reinterpret_cast<Track<KM>*>(full_bar + 4 * kMaxBufs);  // [B][NW][2M]
+  __shared__ ResInfo info_s[kMaxBufs][M];
+  __shared__ int arrive_cnt[kMaxBufs];
+  __shared__ int4 ebuf[kResEdgeBuf];
+  __shared__ int ebuf_n;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+
+  const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
+  if (count <= 0) return;
+  const uint32_t* __restrict__ items = st.use_own ? st.items_own : st.items;
+  const int32_t groups = (count + M - 1) / M;
+  int S = 1;  // segments per item group (short lists): best whole-wave fill
+  {
+    const int G = gridDim.x;
+    float best_eff = -1.f;
+    for (int s = 1; s <= max_segments; ++s) {
+      const long units = static_cast<long>(groups) * s;
+      const long waves = (units + G - 1) / G;
+      const float eff = static_cast<float>(units) / static_cast<float>(waves * G);
+      if (eff > best_eff + 0.04f) {
+        best_eff = eff;
+        S = s;
+      }
+      if (units >= 4L * G) break;
+    }
+  }
+  const int64_t units = static_cast<int64_t>(groups) * S;
+  if (static_cast<int64_t>(blockIdx.x) >= units) return;
+  const int32_t seglen = ((n + S - 1) / S + kBlk - 1) / kBlk * kBlk;
+  const int parity_out = st.ctrl->parity;
+  const int64_t stages = (units - blockIdx.x + gridDim.x - 1) / gridDim.x;  // one per unit
+
+  if (tid == 0) {
+    for (int k = 0; k < bufs; ++k) {
+      mbar_init(&full_bar[k], 1);
+      mbar_init(&empty_bar[k], NW);
+      arrive_cnt[k] = 0;
+    }
+    mbar_init(res_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    ebuf_n = 0;
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------- producer warp ----------------
+    if (lane == 0) {  // resident acur (frozen for the launch)
+      mbar_expect_tx(res_bar, static_cast<uint32_t>(row_bytes));
+      bulk_g2s(acur_s, acur_g, static_cast<uint32_t>(row_bytes), res_bar);
+    }
+    // Item metadata of the next K stages is kept in flight across the warp:
+    // lane l holds item l % M of stage q with q % K == l / M, so each stage's
+    // dependent loads (work list -> tau) were issued K stages earlier and the
+    // TMA issue never waits on them.
+    constexpr int K = 32 / M;
+    auto load_info = [&](int64_t q) -> ResInfo {
+      ResInfo it;
+      it.pad = 0;
+      it.agent = -1;
+      it.job = 0;
+      it.flags = 0;
+      it.sv = 0.0;
+      if (q >= stages || lane >= K * M) return it;
+      const int64_t uq = blockIdx.x + q * gridDim.x;
+      const int32_t idx = static_cast<int32_t>(uq / S) * M + lane % M;
+      if (idx < count) {
+        const uint32_t w = full ? (static_cast<uint32_t>(idx) | kItemAgent | kItemJob) : items[idx];
+        it.agent = static_cast<int32_t>(w & kItemMask);
+        it.job = tau_g[it.agent];
+        it.flags = w & (kItemAgent | kItemJob);
+      }
+      return it;
+    };
+    ResInfo mine = load_info(lane / M);
+    for (int64_t q = 0; q < stages; ++q) {
+      const int b = static_cast<int>(q % bufs);
+      const int src = static_cast<int>(q % K) * M + (lane % M);
+      ResInfo cur;
+      cur.agent = __shfl_sync(0xffffffffu, mine.agent, src);
+      cur.job = __shfl_sync(0xffffffffu, mine.job, src);
+      cur.flags = __shfl_sync(0xffffffffu, mine.flags, src);
+      cur.pad = 0;
+      cur.sv = 0.0;
+      if (lane / M == static_cast<int>(q % K)) mine = load_info(q + K);  // refill this slot
+      if (q >= bufs) mbar_wait(&empty_bar[b], static_cast<uint32_t>(((q / bufs) - 1) & 1));
+      if (lane < M) info_s[b][lane] = cur;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        uint32_t total = 0;
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+          if (info_s[b][m].agent >= 0) total += 2u * static_cast<uint32_t>(row_bytes);
+        mbar_expect_tx(&full_bar[b], total);
+        unsigned char* sb = stage_base + b * stage_bytes;
+        // full sweeps stage M consecutive agents: their A rows are one
+        // contiguous block, copied with a single bulk copy
+        bool contiguous = full != 0;
+#pragma unroll
+        for (int m = 1; m < M; ++m)
+          contiguous = contiguous && info_s[b][m].agent == info_s[b][0].agent + m;
+        if (contiguous) {
+          bulk_g2s(sb, reinterpret_cast<const unsigned char*>(A + static_cast<int64_t>(info_s[b][0].agent) * ld),
+                   static_cast<uint32_t>(M * row_bytes), &full_bar[b]);
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const ResInfo im = info_s[b][m];
+          if (im.agent < 0) continue;
+          if (!contiguous)
+            bulk_g2s(sb + m * row_bytes,
+                     reinterpret_cast<const unsigned char*>(A + static_cast<int64_t>(im.agent) * ld),
+                     static_cast<uint32_t>(row_bytes), &full_bar[b]);
+          bulk_g2s(sb + (M + m) * row_bytes,
+                   reinterpret_cast<const unsigned char*>(AT + static_cast<int64_t>(im.job) * ld),
+                   static_cast<uint32_t>(row_bytes), &full_bar[b]);
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    // resident tau as uint16 (n < 65536 is a precondition of this kernel)
+    for (int32_t i = tid * 4; i < ld; i += NW * 32 * 4) {
+      const int4 v = __ldg(reinterpret_cast<const int4*>(tau_g + i));
+      uint2 w;
+      w.x = (static_cast<uint32_t>(v.x) & 0xFFFFu) | (static_cast<uint32_t>(v.y) << 16);
+      w.y = (static_cast<uint32_t>(v.z) & 0xFFFFu) | (static_cast<uint32_t>(v.w) << 16);
+      *reinterpret_cast<uint2*>(tau_s + i) = w;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    mbar_wait(res_bar, 0);
+
+    Track<KM> ta[M], tj[M];
+    const int32_t nstages = static_cast<int32_t>(stages);
+    int b = 0;
+    uint32_t phase = 0;
+    int32_t uq = blockIdx.x;
+    for (int32_t q = 0; q < nstages; ++q, uq += gridDim.x) {
+      const int32_t group = uq / S;
+      const int32_t seg = uq - group * S;
+      const int32_t seg_lo = seg * seglen;
+      const int32_t seg_hi = min(n, seg_lo + seglen);
+      mbar_wait_sleep(&full_bar[b], phase);
+      Acc sv[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int32_t ag = info_s[b][m].agent;
+        sv[m] = ag >= 0 ? widen(acur_s[ag]) : Acc(0);
+        ta[m].init();
+        tj[m].init();
+      }
+      const E* rowsA = reinterpret_cast<const E*>(stage_base + b * stage_bytes);
+      const E* rowsT = rowsA + static_cast<size_t>(M) * ld;
+
+      if constexpr (KM == kPacked32) {
+        uint32_t ka[M], kj[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          ka[m] = 0u;
+          kj[m] = 0u;
+        }
+        const uint32_t pitch_b = static_cast<uint32_t>(row_bytes);
+        int32_t i0 = seg_lo + warp * kBlk + lane * V;
+        for (; i0 + V <= seg_hi; i0 += kStride) {
+          const uint4 tw = *reinterpret_cast<const uint4*>(tau_s + i0);
+          const uint4 cw = *reinterpret_cast<const uint4*>(acur_s + i0);
+          uint4 xw[M];
+#pragma unroll
+          for (int m = 0; m < M; ++m) xw[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
+          res_step_p32<M>(tw, cw, xw, i0, reinterpret_cast<const char*>(rowsA), pitch_b, ka, kj);
+        }
+        // keys -> tracks with s restored (packed32 keys carry d' = d + s)
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const uint32_t sh = static_cast<uint32_t>(sv[m]) * 16384u;
+          ta[m].k = ka[m] ? ka[m] - sh : 0u;
+          tj[m].k = kj[m] ? kj[m] - sh : 0u;
+        }
+        if (i0 < seg_hi) {  // ragged tail (n % 8 != 0): generic body
+          StreamRegs<E, M> r;
+          lds_tau<E>(tau_s + i0, r.t);
+          r.c = *reinterpret_cast<const uint4*>(acur_s + i0);
+#pragma unroll
+          for (int m = 0; m < M; ++m) r.x[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
+          compute_step<E, M, KM, false>(r, i0, seg_hi - i0, rowsA, ld, 0, sv, ta, tj);
+        }
+      } else {
+        for (int32_t i0 = seg_lo + warp * kBlk + lane * V; i0 < seg_hi; i0 += kStride) {
+          StreamRegs<E, M> r;
+          lds_tau<E>(tau_s + i0, r.t);
+          r.c = *reinterpret_cast<const uint4*>(acur_s + i0);
+#pragma unroll
+          for (int m = 0; m < M; ++m) r.x[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
+          if (i0 + V <= seg_hi)  // whole vector: branch-free body, gathers overlap
+            compute_step<E, M, KM, false>(r, i0, V, rowsA, ld, 0, sv, ta, tj);
+          else
+            compute_step<E, M, KM, false>(r, i0, seg_hi - i0, rowsA, ld, 0, sv, ta, tj);
+        }
+      }
+
+      // warp partials -> red[b]; the last warp to arrive reduces and writes
+      Track<KM>* rq = red + b * NW * 2 * M;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        ta[m].warp_reduce();
+        tj[m].warp_reduce();
+        if (lane == 0) {
+          rq[warp * 2 * M + 2 * m] = ta[m];
+          rq[warp * 2 * M + 2 * m + 1] = tj[m];
+        }
+      }
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&arrive_cnt[b], 1) == NW - 1;
+        if (last) arrive_cnt[b] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence_block();
+        Track<KM> r;
+        r.init();
+        if (lane < 2 * M)
+          for (int w = 0; w < NW; ++w) r.merge(rq[w * 2 * M + lane]);
+        bool finalize = (S == 1);
+        double d = 0.0;
+        int32_t k = -1;
+        bool ok = false;
+        if (S == 1) {
+          ok = lane < 2 * M && r.valid();
+          d = ok ? r.delta() : 0.0;
+          k = ok ? r.index() : -1;
+        } else {
+          // publish this segment's partials; the last segment to arrive combines
+          if (lane < 2 * M) {
+            const int64_t slot = (static_cast<int64_t>(group) * S + seg) * M + (lane >> 1);
+            const double pd = r.valid() ? r.delta() : -__longlong_as_double(0x7ff0000000000000ll);
+            const int32_t pk = r.valid() ? r.index() : INT_MAX;
+            if ((lane & 1) == 0) {
+              st.part_ad[slot] = pd;
+              st.part_at[slot] = pk;
+            } else {
+              st.part_jd[slot] = pd;
+              st.part_ji[slot] = pk;
+            }
+          }
+          __threadfence();
+          __syncwarp();
+          int lastseg = 0;
+          if (lane == 0) {
+            lastseg = atomicAdd(&st.part_arrive[group], 1) == S - 1;
+            if (lastseg) st.part_arrive[group] = 0;
+          }
+          finalize = __shfl_sync(0xffffffffu, lastseg, 0);
+          if (finalize) {
+            __threadfence();
+            Track<kFloat> c;
+            c.init();
+            if (lane < 2 * M)
+              for (int s2 = 0; s2 < S; ++s2) {
+                const int64_t slot = (static_cast<int64_t>(group) * S + s2) * M + (lane >> 1);
+                Track<kFloat> o;
+                o.d = (lane & 1) ? __ldcg(&st.part_jd[slot]) : __ldcg(&st.part_ad[slot]);
+                o.i = (lane & 1) ? __ldcg(&st.part_ji[slot]) : __ldcg(&st.part_at[slot]);
+                c.merge(o);
+              }
+            ok = lane < 2 * M && c.valid();
+            d = c.d;
+            k = c.i;
+          }
+        }
+        if (finalize) {
+          bool emit = false;
+          int4 entry = make_int4(0, 0, 0, 0);
+          if (lane < 2 * M) {
+            const ResInfo im = info_s[b][lane >> 1];
+            const bool active = ok && d > st.eps;
+            if (im.agent >= 0) {
+              if ((lane & 1) == 0) {
+                if (im.flags & kItemAgent) {
+                  st.agent_delta[im.agent] = active ? d : 0.0;
+                  st.agent_partner[im.agent] = active ? k : -1;
+                  emit = active && st.emit_edges;
+                  entry = make_int4(im.agent, im.agent, k, im.job);
+                }
+              } else if (im.flags & kItemJob) {
+                st.job_delta[im.job] = active ? d : 0.0;
+                st.job_partner[im.job] = active ? k : -1;
+                emit = active && st.emit_edges;
+                entry = make_int4(n + im.job, im.agent, k, im.job);
+              }
+            }
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, emit);
+          if (mask) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&ebuf_n, __popc(mask));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (emit) {
+              const int pos = base + __popc(mask & ((1u << lane) - 1));
+              if (pos < kResEdgeBuf) {
+                ebuf[pos] = entry;
+              } else {  // overflow: direct global append
+                const int g = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
+                st.edges[parity_out][g] = entry;
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[b]);
+      if (++b == bufs) {
+        b = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+  // flush the CTA's buffered edges
+  __syncthreads();
+  const int ne = min(ebuf_n, kResEdgeBuf);
+  __shared__ int gbase;
+  if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
+  __syncthreads();
+  for (int e = tid; e < ne; e += kResThreads) st.edges[parity_out][gbase + e] = ebuf[e];
+}
+
+// Dynamic smem of the resident kernel for (ld, elem size, M, bufs).
+inline size_t res_smem_bytes(int64_t ld, size_t es, int M, int bufs) {
+  const size_t row = static_cast<size_t>(ld) * es;
+  const size_t tau = (static_cast<size_t>(ld) * 2 + 127) / 128 * 128;
+  const size_t acur = (row + 127) / 128 * 128;
+  return tau + acur + static_cast<size_t>(bufs) * 2 * M * row + 4 * kMaxBufs * 8 +
+         static_cast<size_t>(bufs) * kResWarps * 2 * M * 16;
+}
+
+template <class E, int M, int KM>
+cudaError_t launch_res_m(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  auto k = pair_scan_res_kernel<E, M, KM>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(p.smem));
+  if (e != cudaSuccess) return e;
+  k<<<p.ctas, kResThreads, p.smem, st>>>(d, full, p.bufs, p.max_segments);
+  return cudaGetLastError();
+}
+
+template <class E, int KM>
+cudaError_t launch_res(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  switch (p.m) {
+    case 1: return launch_res_m<E, 1, KM>(d, p, full, st);
+    case 2: return launch_res_m<E, 2, KM>(d, p, full, st);
+    case 4: return launch_res_m<E, 4, KM>(d, p, full, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace scan_detail
+
+template <class E, int KM>
+cudaError_t launch_scan_res_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  return scan_detail::launch_res<E, KM>(d, p, full, st);
+}
+
+}  // namespace lsapgpu

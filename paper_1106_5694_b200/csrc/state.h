@@ -103,6 +103,7 @@ struct ScanPlan {
   int threads = 256;
   size_t smem = 0;      // dynamic smem per CTA
   int max_segments = 1;
+  int resident = 0;     // 1: resident-state kernel (scan_resident.cuh)
 };
 ScanPlan plan_scan(const DevState& d, int num_sms);
 // full sweep (identity work list, count n) when full != 0, else the device work list

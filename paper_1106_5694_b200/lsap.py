@@ -463,6 +463,18 @@ _ctx_lock = threading.Lock()
 _contexts: dict = {}
 
 
+def generate_instance(kind: str, n: int, seed: int = 0, param: Optional[float] = None,
+                      device: int = 0) -> np.ndarray:
+    """Synthetic instance (SURVEY 8(d) recipes) built by the on-device generator
+    and returned as the reference's host fp64 row-major matrix (n x n)."""
+    ctx = Context(device)
+    try:
+        ctx.generate(kind, n, seed, param)
+        return ctx.read_rows(np.arange(n, dtype=np.int32))
+    finally:
+        ctx.close()
+
+
 def context(device: int = 0) -> Context:
     """Process-wide default context per device (like the reference's private pool per call)."""
     with _ctx_lock:

@@ -111,12 +111,18 @@ def test_generators_match_oracle(oracle, gpu_ctx):
 
 
 @pytest.mark.parametrize("env", [
-    {"LSAPGPU_SCAN_M": "1"}, {"LSAPGPU_SCAN_M": "2"}, {"LSAPGPU_SCAN_M": "4"},
-    {"LSAPGPU_SCAN_BUDGET": "3072"},                                   # 4 passes, single buffer
-    {"LSAPGPU_SCAN_BUDGET": "9000", "LSAPGPU_SCAN_M": "1"},            # single-buffered rows
-    {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # split items over CTAs
-    {"LSAPGPU_SCAN_NT": "512", "LSAPGPU_SCAN_BUFS": "2"},               # double-buffered ring
-    {"LSAPGPU_SCAN_NT": "512", "LSAPGPU_SCAN_BUFS": "4", "LSAPGPU_SCAN_M": "1"},  # 4-deep ring
+    {},                                                                # resident-state kernel (default)
+    {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
+    {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
+    {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "1"},             # streaming kernel
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "2"},
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "4"},
+    {"LSAPGPU_SCAN_BUDGET": "3072"},                                   # streaming, chunked passes
+    {"LSAPGPU_SCAN_BUDGET": "9000", "LSAPGPU_SCAN_M": "1"},            # streaming, single-buffered rows
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_SEGMENTS": "8"},      # streaming, split items
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_NT": "512", "LSAPGPU_SCAN_BUFS": "2"},
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_NT": "512", "LSAPGPU_SCAN_BUFS": "4", "LSAPGPU_SCAN_M": "1"},
 ])
 def test_scan_plan_variants_subprocess(env):
     """Every scan-plan code path (batching, chunked passes, segments) is bit-exact.
@@ -128,7 +134,7 @@ def test_scan_plan_variants_subprocess(env):
         "import paper_1106_5694_b200 as g\n"
         "from oracle.oracle import Oracle\n"
         "o = Oracle(); ctx = g.Context(0)\n"
-        "for kind, n in [('f32', 1000), ('int', 700), ('geom', 300)]:\n"
+        "for kind, n in [('f32', 1000), ('int', 700), ('geom', 300), ('p2p', 1001), ('int', 2500)]:\n"
         "    a = o.generate(kind, n, 11); s = o.random_perm(n, 4)\n"
         "    ctx.set_matrix(a); t = ctx.evaluate_all(s)\n"
         "    ad, ap, jd, jp = o.evaluate_all(a, s)\n"

@@ -21,7 +21,12 @@ for kind, n in %s:
 print(json.dumps(out))
 '''
 cases = sys.argv[1] if len(sys.argv) > 1 else "[('p2p', 10000), ('f32', 10000)]"
-for nt, m, b in [(512, 4, 2), (256, 4, 1), (256, 4, 2), (256, 2, 2), (256, 2, 1), (512, 4, 1)]:
-    env = dict(os.environ, LSAPGPU_SCAN_M=str(m), LSAPGPU_SCAN_BUFS=str(b), LSAPGPU_SCAN_NT=str(nt))
+grid = [(256, 4, 1, 2), (256, 4, 1, 3), (256, 2, 1, 3), (256, 2, 2, 2), (256, 2, 2, 3), (256, 2, 2, 4),
+        (256, 4, 2, 2), (256, 4, 2, 3), (256, 1, 2, 3), (256, 1, 2, 4)]
+if len(sys.argv) > 2:
+    grid = json.loads(sys.argv[2])
+for nt, m, b, dd in grid:
+    env = dict(os.environ, LSAPGPU_SCAN_M=str(m), LSAPGPU_SCAN_BUFS=str(b), LSAPGPU_SCAN_NT=str(nt),
+               LSAPGPU_SCAN_DEPTH=str(dd))
     r = subprocess.run([sys.executable, "-c", code % (ROOT, cases)], env=env, capture_output=True, text=True)
-    print(f"NT={nt} M={m} B={b}", r.stdout.strip() or r.stderr[-500:], flush=True)
+    print(f"NT={nt} M={m} B={b} D={dd}", r.stdout.strip() or r.stderr[-500:], flush=True)

@@ -44,7 +44,12 @@ def main(rep, obj, kernel_sub, top=40):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    recs = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+    recs = []
+    for r in rows[2:]:
+        if r and r[0] == "Kernel Name" and recs:
+            break  # only the first captured launch
+        if len(r) == len(hdr) and r[0].startswith("0x"):
+            recs.append(dict(zip(hdr, r)))
     base = int(recs[0]["Address"], 16)
     agg = collections.Counter()
     src = {}
