@@ -195,6 +195,14 @@ int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launc
                         double* full_sweep_ms, int64_t* full_sweeps, double* commit_ms,
                         int64_t* commit_launches);
 
+/* Device timeline (instrumentation, off by default): with capacity > 0 the
+ * first CTA of every pair-scan and commit launch appends one entry
+ * (%globaltimer ns << 4 | kind: 1 full sweep, 2 re-evaluation scan, 3 commit
+ * start, 4 commit end) so graph-mode solves can be broken down by phase.
+ * lsapgpu_timeline copies out and clears the entries; returns the count. */
+int lsapgpu_set_timeline(lsapgpu_ctx* ctx, int32_t capacity);
+int32_t lsapgpu_timeline(lsapgpu_ctx* ctx, uint64_t* out, int32_t capacity);
+
 #ifdef __cplusplus
 }
 #endif

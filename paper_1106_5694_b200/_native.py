@@ -27,6 +27,7 @@ EXPORTS = [
     "lsapgpu_evaluate_all", "lsapgpu_check_conflicts", "lsapgpu_apply_parallel_switches",
     "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_solve_dist",
     "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
+    "lsapgpu_set_timeline", "lsapgpu_timeline",
 ]
 
 
@@ -112,6 +113,8 @@ def _load() -> C.CDLL:
                                          i64, C.POINTER(i64)]),
         "lsapgpu_dist_exchange_bytes": (C.c_size_t, [i32, i32]),
         "lsapgpu_set_scan_timing": (C.c_int, [vp, C.c_int]),
+        "lsapgpu_set_timeline": (C.c_int, [vp, C.c_int32]),
+        "lsapgpu_timeline": (C.c_int32, [vp, C.c_void_p, C.c_int32]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
                                           C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),
     }

@@ -21,8 +21,11 @@
 // earlier neighbour (every earlier neighbour was rejected by an earlier
 // accepted edge), so by induction the accepted set, the rejected set and hence
 // reserved / conflicted / conflicted_jobs equal the sequential walk's.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
+#include "commit_single.cuh"
 #include "state.h"
 
 namespace lsapgpu {
@@ -31,28 +34,30 @@ namespace {
 constexpr uint8_t kEdgeCommitted = 4;
 
 __global__ void tau_from_sigma_kernel(DevState st) {
-  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < st.n; j += gridDim.x * blockDim.x)
+  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < st.n; j += gridDim.x * blockDim.x) {
     st.tau[st.sigma[j]] = j;
+    if (st.tau16) st.tau16[st.sigma[j]] = static_cast<uint16_t>(j);
+  }
 }
 
-// every slot with delta > 0 and partner >= 0 becomes a proposal entry
+// every slot with delta > 0 and partner >= 0 becomes a proposal entry (the
+// step APIs check conflicts without an instance: no entries of A are read;
+// apply_kernel recomputes the exchanges from the instance it is given)
 __global__ void edges_from_tables_kernel(DevState st) {
   const int32_t n = st.n;
   const int P = st.ctrl->parity;
   for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < 2 * n; s += gridDim.x * blockDim.x) {
-    int4 en;
-    bool active;
     if (s < n) {
-      active = st.agent_partner[s] >= 0 && st.agent_delta[s] > 0.0;
-      en = make_int4(s, s, st.agent_partner[s], st.tau[s]);
+      if (!(st.agent_partner[s] >= 0 && st.agent_delta[s] > 0.0)) continue;
+      const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
+      st.edges[P][pos] = agent_prop(st.sigma, st.tau, nullptr, st.storage, st.ld, s, st.agent_partner[s],
+                                    st.agent_delta[s]);
     } else {
       const int32_t j = s - n;
-      active = st.job_partner[j] >= 0 && st.job_delta[j] > 0.0;
-      en = make_int4(s, st.sigma[j], st.job_partner[j], j);
-    }
-    if (active) {
+      if (!(st.job_partner[j] >= 0 && st.job_delta[j] > 0.0)) continue;
       const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
-      st.edges[P][pos] = en;
+      st.edges[P][pos] = job_prop(st.sigma, st.tau, nullptr, st.storage, st.ld, n, j, st.job_partner[j],
+                                  st.job_delta[j]);
     }
   }
 }
@@ -69,13 +74,13 @@ __global__ void __launch_bounds__(1024, 1)
   const int64_t ld = st.ld;
   const int P = C->parity;
   const int32_t m = C->edge_count[P];
-  const int4* edges = st.edges[P];
+  const Prop* edges = st.edges[P];
   const int32_t iter = C->iter + 1;
   if (tid == 0) s_committed = 0;
 
   // select on the frozen assignment
   for (int32_t e = tid; e < m; e += NT) {
-    const int4 en = edges[e];
+    const int4 en = prop_key(edges[e], n);
     st.estate[e] = kEdgeUndecided;
     if (!(en.x < n ? acc_agent[en.x] : acc_job[en.x - n])) continue;
     int32_t agent, j_new, j_old, disp;
@@ -120,10 +125,14 @@ __global__ void __launch_bounds__(1024, 1)
     st.sigma[j_old] = disp;
     st.tau[agent] = j_new;
     st.tau[disp] = j_old;
+    if (st.tau16) {
+      st.tau16[agent] = static_cast<uint16_t>(j_new);
+      st.tau16[disp] = static_cast<uint16_t>(j_old);
+    }
     acur[agent] = A[static_cast<int64_t>(agent) * ld + j_new];
     acur[disp] = A[static_cast<int64_t>(disp) * ld + j_old];
     const unsigned long long pos = atomicAdd(reinterpret_cast<unsigned long long*>(&C->log_count), 1ull);
-    st.log[pos] = LogEntry{iter, edges[e].x, st.c_delta[e]};
+    st.log[pos] = LogEntry{iter, edges[e].slot, st.c_delta[e]};
     ++local;
   }
   if (local) atomicAdd(&s_committed, local);
@@ -134,7 +143,74 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// Grid-wide second half of the split commit (commit_single.cuh): apply the
+// committed exchanges in any order (they are disjoint), append their delta-log
+// entries at the reserved positions (the host orders the log by (iter,
+// slot)), and write the re-evaluation items: both agents of every committed
+// exchange, then every queued conflicted proposer with its job when the job's
+// own record was rejected (parallel.cpp:296-330).
+template <class E>
+__global__ void __launch_bounds__(256) commit_apply_kernel(DevState st) {
+  Ctrl* C = st.ctrl;
+  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark(C, st.tl, st.tl_cap, 15);
+  const int32_t nlog = C->k2_nlog, nconf = C->k2_nconf;
+  if (nlog + nconf == 0) return;
+  const int32_t n = st.n;
+  const Prop* edges = st.edges[C->k2_parity];
+  const int32_t iter = C->k2_iter;
+  const int64_t base = C->k2_log_base;
+  E* acur = static_cast<E*>(st.acur);
+  int jobs = 0;
+  for (int32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nlog + nconf; x += gridDim.x * blockDim.x) {
+    if (x < nlog) {
+      const Prop p = edges[st.clist[x]];
+      if (p.slot < n) {
+        st.agent_delta[p.a] = 0.0;
+        st.agent_partner[p.a] = -1;
+      } else {
+        st.job_delta[p.j_new] = 0.0;
+        st.job_partner[p.j_new] = -1;
+      }
+      st.sigma[p.j_new] = p.a;
+      st.sigma[p.j_old] = p.d;
+      st.tau[p.a] = p.j_new;
+      st.tau[p.d] = p.j_old;
+      if (st.tau16) {
+        st.tau16[p.a] = static_cast<uint16_t>(p.j_new);
+        st.tau16[p.d] = static_cast<uint16_t>(p.j_old);
+      }
+      acur[p.a] = static_cast<E>(p.acur_a);
+      acur[p.d] = static_cast<E>(p.acur_d);
+      st.log[base + x] = LogEntry{iter, p.slot, p.delta};
+      st.items[2 * x] = static_cast<uint32_t>(p.a) | kItemAgent | kItemJob;
+      st.items[2 * x + 1] = static_cast<uint32_t>(p.d) | kItemAgent | kItemJob;
+    } else {
+      const int32_t q = x - nlog;
+      const Prop p = edges[st.qlist[q]];
+      const int32_t owner = p.slot < n ? p.a : p.d;
+      const int32_t job = p.slot < n ? p.j_old : p.j_new;  // the owner's (unchanged) job
+      const bool jflag = (st.jbits[job >> 5] >> (job & 31)) & 1u;
+      st.items[2 * nlog + q] = static_cast<uint32_t>(owner) | kItemAgent | (jflag ? kItemJob : 0u);
+      jobs += jflag;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) jobs += __shfl_down_sync(0xffffffffu, jobs, off);
+  if ((threadIdx.x & 31) == 0 && jobs)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&C->job_scans), static_cast<unsigned long long>(jobs));
+}
+
 }  // namespace
+
+cudaError_t launch_commit_apply(const DevState& d, cudaStream_t st) {
+  switch (d.storage) {
+    case kI16: commit_apply_kernel<int16_t><<<64, 256, 0, st>>>(d); break;
+    case kI32: commit_apply_kernel<int32_t><<<64, 256, 0, st>>>(d); break;
+    case kF32: commit_apply_kernel<float><<<64, 256, 0, st>>>(d); break;
+    case kF64: commit_apply_kernel<double><<<64, 256, 0, st>>>(d); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 CommitPlan plan_commit(const DevState& d) {
   CommitPlan p;
@@ -145,13 +221,36 @@ CommitPlan plan_commit(const DevState& d) {
   const size_t kslice = ((static_cast<size_t>(d.n) + p.cluster - 1) / p.cluster * 4 + 15) / 16 * 16;
   const size_t cap = budget > 2 * kslice + 64 ? (budget - 2 * kslice - 64) / 45 : 0;
   p.edge_cap = static_cast<int>(cap / 16 * 16);
+  // split commit (commit_single.cuh): per-agent keys + rejected-job bitmap,
+  // 13 B per proposal, in one CTA's shared memory
+  // One SM's load/store throughput makes the split commit slower than the
+  // cluster for the large early batches; it wins below a few thousand
+  // proposals (measured on B200, C2/C3: 2k-6k best).
+  p.cta_edge_cap = std::min(single::edge_capacity(d.n, budget), 4096);
+  if (p.cta_edge_cap < 1024) p.cta_edge_cap = 0;
+  if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE"))
+    if (std::atoi(s) == 0) p.cta_edge_cap = 0;
+  if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE_MAX")) p.cta_edge_cap = std::min(p.cta_edge_cap, std::atoi(s));
   return p;
 }
 
 cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
                           cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st) {
   if (mode == kCommitApplyOnly) return cudaErrorInvalidValue;  // launch_accepted_from_masks
-  return launch_commit_cluster(d, p, mode, cond, use_cond, st);
+  cudaError_t e = launch_commit_cluster(d, p, mode, cond, use_cond, st);
+  if (e != cudaSuccess || mode != kCommitSolve) return e;
+  return launch_commit_apply(d, st);
+}
+
+__global__ void tau16_sync_kernel(DevState st) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += gridDim.x * blockDim.x)
+    st.tau16[i] = static_cast<uint16_t>(st.tau[i]);
+}
+
+cudaError_t launch_tau16_sync(const DevState& d, cudaStream_t st) {
+  if (!d.tau16) return cudaSuccess;
+  tau16_sync_kernel<<<64, 256, 0, st>>>(d);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_edges_from_tables(const DevState& d, cudaStream_t st) {

@@ -30,6 +30,7 @@
 
 #include <climits>
 
+#include "commit_single.cuh"
 #include "state.h"
 
 namespace cg = cooperative_groups;
@@ -74,7 +75,7 @@ struct EdgeArrays {
 template <class E, int CS>
 __global__ void __launch_bounds__(kNT, 1)
     commit_cluster_kernel(DevState st, int mode, cudaGraphConditionalHandle cond, int use_cond,
-                          int edge_cap) {
+                          int edge_cap, int cta_cap) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x;
@@ -90,8 +91,9 @@ __global__ void __launch_bounds__(kNT, 1)
   const int64_t ld = st.ld;
   const int P = C->parity;
   const int32_t m = C->edge_count[P];
-  const int4* edges = st.edges[P];
+  const Prop* edges = st.edges[P];
 
+  if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, kTlCommit);
   // ---- P0: control ----
   if (mode == kCommitSolve) {
     int abort = 0;
@@ -106,11 +108,20 @@ __global__ void __launch_bounds__(kNT, 1)
         if (abort == 2) C->inner_done = 1;
         if (abort == 4) C->drain = 1;
         C->work_count = 0;
+        C->k2_nlog = C->k2_nconf = 0;
         if (use_cond) cudaGraphSetConditional(cond, 0);
       }
       return;
     }
     if (rank == 0 && tid == 0) C->work_count = 0;  // appends start after two cluster barriers
+  }
+  // Default policy and a batch whose vertex state fits one SM: the conflict
+  // check runs on one CTA with CTA barriers and local shared-memory atomics,
+  // and the scattered writes follow grid-wide in commit_apply_kernel
+  // (commit_single.cuh).  Otherwise the whole cluster runs the iteration.
+  if (m <= cta_cap && (st.policy == 0 || mode == kCommitCheckOnly)) {
+    if (rank == 0) single::commit_single(st, mode, cta_cap, smem);
+    return;
   }
   const int32_t iter = C->iter + 1;
 
@@ -167,7 +178,7 @@ __global__ void __launch_bounds__(kNT, 1)
   }
   for (int32_t l = tid; l < cnt; l += kNT) {
     // proposals carry {slot, proposer, partner, job}: one dependent load left
-    const int4 en = edges[e0 + l];
+    const int4 en = prop_key(edges[e0 + l], n);
     Ea.u[l] = en.y;  // proposer: the agent, or the job's current holder (frozen)
     if (en.x < n) {
       Ea.v[l] = st.sigma[en.z];  // the displaced holder of the proposed job
@@ -181,6 +192,7 @@ __global__ void __launch_bounds__(kNT, 1)
     Ea.slot[l] = en.x;
   }
   cluster.sync();
+  if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 11);
 
   // ---- P2: LFMM rounds ----
   uint32_t R = 1;
@@ -231,6 +243,7 @@ __global__ void __launch_bounds__(kNT, 1)
       }
     }
     cluster.sync();
+    if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 12);
     ++R;
     ++rounds;
   }
@@ -253,12 +266,12 @@ __global__ void __launch_bounds__(kNT, 1)
   for (int32_t l = tid; l < cnt; l += kNT) {
     const uint8_t s = Ea.st[l];
     if (s == kEdgeRejected) {
-      const int4 en = edges[e0 + l];
+      const int4 en = prop_key(edges[e0 + l], n);
       if (en.x >= n) atomicOr(fbase[en.w % CS] + en.w / CS, kJobRejected);
       continue;
     }
     if (s != kEdgeAccepted) continue;
-    const int4 en = edges[e0 + l];
+    const int4 en = prop_key(edges[e0 + l], n);
     int32_t agent, j_new, disp;
     const int32_t j_old = Ea.jold[l];
     if (en.x < n) {  // agent_proposal_delta, solver_state.hpp:106-113
@@ -294,23 +307,28 @@ __global__ void __launch_bounds__(kNT, 1)
   }
   if (overlap) atomicExch(&C->error, 1);
   cluster.sync();
+  if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 13);
 
   // ---- P4: apply, then rank log entries and work items ----
   for (int32_t l = tid; l < cnt; l += kNT) {
     const uint8_t s = Ea.st[l];
     if (s == kEdgeCommitted) {
       const int32_t agent = Ea.u[l], disp = Ea.v[l], j_old = Ea.jold[l];
-      const int4 en = edges[e0 + l];
+      const int4 en = prop_key(edges[e0 + l], n);
       const int32_t j_new = en.x < n ? en.z : en.w;
       st.sigma[j_new] = agent;
       st.sigma[j_old] = disp;
       st.tau[agent] = j_new;
       st.tau[disp] = j_old;
+      if (st.tau16) {
+        st.tau16[agent] = static_cast<uint16_t>(j_new);
+        st.tau16[disp] = static_cast<uint16_t>(j_old);
+      }
       acur[agent] = static_cast<E>(Ea.acur_a[l]);
       acur[disp] = static_cast<E>(Ea.acur_d[l]);
       Ea.rank[l] = atomicAdd(&sc.nlog, 1);
     } else if (s == kEdgeRejected) {
-      const int4 en = edges[e0 + l];
+      const int4 en = prop_key(edges[e0 + l], n);
       const int32_t p = en.y;  // the proposer (frozen holder for job-side proposals)
       uint32_t* fp = fbase[p % CS] + p / CS;
       if (st.policy == 0) {
@@ -323,7 +341,7 @@ __global__ void __launch_bounds__(kNT, 1)
       } else if (!(*fp & kTouched)) {
         // touched_only: an untouched proposer keeps its stale record -> carry it
         const int pos = atomicAdd(&C->edge_count[1 - P], 1);
-        st.edges[1 - P][pos] = en;
+        st.edges[1 - P][pos] = edges[e0 + l];
       }
     }
   }
@@ -349,17 +367,19 @@ __global__ void __launch_bounds__(kNT, 1)
     const int32_t r = Ea.rank[l];
     if (r == kNoEmit) continue;
     if (Ea.st[l] == kEdgeCommitted) {
-      st.log[blog + r] = LogEntry{iter, edges[e0 + l].x, Ea.del[l]};
+      st.log[blog + r] = LogEntry{iter, edges[e0 + l].slot, Ea.del[l]};
       st.items[bitems + 2 * r] = static_cast<uint32_t>(Ea.u[l]) | kItemAgent | kItemJob;
       st.items[bitems + 2 * r + 1] = static_cast<uint32_t>(Ea.v[l]) | kItemAgent | kItemJob;
     } else {
-      const int32_t p = edges[e0 + l].y;
+      const int32_t p = prop_key(edges[e0 + l], n).y;
       st.items[bitems + nlog2 + (r & ~kJobFlagBit)] =
           static_cast<uint32_t>(p) | kItemAgent | ((r & kJobFlagBit) ? kItemJob : 0u);
     }
   }
+  if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 14);
   cluster.sync();  // every peer is done with this CTA's shared memory
   if (rank == 0 && tid == 0) {
+    C->k2_nlog = C->k2_nconf = 0;  // the apply kernel has nothing left to do
     C->iter = iter;
     C->parity = 1 - P;
     C->edge_count[P] = 0;
@@ -367,6 +387,7 @@ __global__ void __launch_bounds__(kNT, 1)
     C->inner_iterations += 1;
     // anytime deadline, acted on by the next commit (solver_state.hpp:13-27)
     if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
+    tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
   }
 }
 
@@ -393,7 +414,7 @@ cudaError_t launch_cs(const DevState& d, const CommitPlan& p, int mode, cudaGrap
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap);
+  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap);
 }
 
 template <int CS>

@@ -100,12 +100,98 @@ struct Ctrl {
   int64_t lfmm_rounds;      // total LFMM rounds (instrumentation)
   int64_t inner_iterations; // batches (this solve)
   uint64_t deadline_gt;     // %globaltimer deadline, 0 = none
+  int32_t tl_count;         // device timeline entries (instrumentation)
+  // conflict-check -> apply hand-off of the split commit (commit_single.cuh,
+  // commit_apply): committed / queued-conflicted proposal lists of one batch
+  int32_t k2_parity, k2_nlog, k2_nconf, k2_iter;
+  int64_t k2_log_base;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// One active record as a proposal for the conflict check, written by the
+// producer of the record (the pair scan, the multi-GPU record merge, the
+// step-API table import) against the state the record was computed on.  The
+// exchange moves agent a to job j_new and the displaced agent d to job j_old:
+//   agent record of i (slot i, partner job k):   a = i, d = sigma[k],
+//                                                j_new = k, j_old = tau[i]
+//   job record of j (slot n + j, partner k):     a = k, d = sigma[j],
+//                                                j_new = j, j_old = tau[k]
+// delta is the record's value; acur_a = A[a][j_new] and acur_d = A[d][j_old]
+// are the two entries the apply writes (exact in fp64 for every storage).
+struct Prop {
+  int32_t slot;
+  int32_t a, d;
+  int32_t j_new, j_old;
+  int32_t pad;
+  double delta;
+  double acur_a, acur_d;
+};
+static_assert(sizeof(Prop) == 48, "proposal layout");
+
+// The compact {slot, proposer, partner, job} view the general commit path
+// uses: proposer = the record's owner (i, or the holder of j), partner = the
+// record's partner (job k, or agent k), job = the owner's current job.
+__device__ __forceinline__ int4 prop_key(const Prop& p, int32_t n) {
+  return p.slot < n ? make_int4(p.slot, p.a, p.j_new, p.j_old) : make_int4(p.slot, p.d, p.a, p.j_new);
+}
+
+// A[i][j] widened to fp64 for any storage type (exact)
+__device__ __forceinline__ double mat_at(const void* M, int storage, int64_t ld, int32_t i, int32_t j) {
+  const int64_t k = static_cast<int64_t>(i) * ld + j;
+  switch (storage) {
+    case kI16: return static_cast<double>(static_cast<const int16_t*>(M)[k]);
+    case kI32: return static_cast<double>(static_cast<const int32_t*>(M)[k]);
+    case kF32: return static_cast<double>(static_cast<const float*>(M)[k]);
+    default: return static_cast<const double*>(M)[k];
+  }
+}
+
+// Proposal of agent i's record (partner job k) / job j's record (partner
+// agent k) on the current state; used by producers that do not hold the rows.
+__device__ __forceinline__ Prop agent_prop(const int32_t* sigma, const int32_t* tau, const void* A, int storage,
+                                           int64_t ld, int32_t i, int32_t k, double delta) {
+  const int32_t d = sigma[k], jo = tau[i];
+  if (A == nullptr) return Prop{i, i, d, k, jo, 0, delta, 0.0, 0.0};  // conflict check only
+  return Prop{i, i, d, k, jo, 0, delta, mat_at(A, storage, ld, i, k), mat_at(A, storage, ld, d, jo)};
+}
+__device__ __forceinline__ Prop job_prop(const int32_t* sigma, const int32_t* tau, const void* A, int storage,
+                                         int64_t ld, int32_t n, int32_t j, int32_t k, double delta) {
+  const int32_t h = sigma[j], jo = tau[k];
+  if (A == nullptr) return Prop{n + j, k, h, j, jo, 0, delta, 0.0, 0.0};  // conflict check only
+  return Prop{n + j, k, h, j, jo, 0, delta, mat_at(A, storage, ld, k, j), mat_at(A, storage, ld, h, jo)};
+}
+
+// Proposal fields a scan defers to the end of its launch (pad != 0) so the
+// dependent global loads do not sit on a stage's critical path: pad 1 = the
+// agent record's displaced holder and its entry, pad 2 = every entry-derived
+// field (the streaming kernel, whose AT rows are not on chip).
+__device__ __forceinline__ Prop finish_prop(Prop p, const int32_t* sigma, const int32_t* tau, const void* A,
+                                            int storage, int64_t ld, int32_t n) {
+  if (p.pad == 0) return p;
+  if (p.slot < n) {  // agent i = a -> job k = j_new; displaced sigma[k] -> j_old = tau[i]
+    p.d = sigma[p.j_new];
+    p.acur_d = mat_at(A, storage, ld, p.d, p.j_old);
+    if (p.pad == 2) p.acur_a = mat_at(A, storage, ld, p.a, p.j_new);
+  } else {  // agent k = a -> job j0 = j_new; holder i = d -> tau[k]
+    p.j_old = tau[p.a];
+    p.acur_a = mat_at(A, storage, ld, p.a, p.j_new);
+    p.acur_d = mat_at(A, storage, ld, p.d, p.j_old);
+  }
+  p.pad = 0;
+  return p;
+}
+
+// timeline kinds
+constexpr unsigned kTlScanFull = 1, kTlScan = 2, kTlCommit = 3, kTlCommitEnd = 4;
+__device__ __forceinline__ void tl_mark(Ctrl* c, unsigned long long* tl, int cap, unsigned kind) {
+  if (tl == nullptr) return;
+  const int i = atomicAdd(&c->tl_count, 1);
+  if (i < cap) tl[i] = (globaltimer() << 4) | kind;
 }
 
 }  // namespace lsapgpu

@@ -56,8 +56,8 @@ __global__ void pack_kernel(DevState st, unsigned char* send) {
   }
 }
 
-// Write every rank's records and append the active ones as proposals
-// {slot, proposer, partner, job} (the layout the pair scan emits).
+// Write every rank's records and append the active ones as proposals (Prop,
+// the layout the pair scan emits).
 __global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t world, size_t bytes_per_rank) {
   const int32_t n = st.n;
   const int P = st.ctrl->parity;
@@ -74,7 +74,8 @@ __global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t wor
         st.agent_partner[i] = rec.agent_partner;
         if (rec.agent_partner >= 0) {
           const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
-          st.edges[P][pos] = make_int4(i, i, rec.agent_partner, rec.job >= 0 ? rec.job : st.tau[i]);
+          st.edges[P][pos] = agent_prop(st.sigma, st.tau, st.A, st.storage, st.ld, i, rec.agent_partner,
+                                        rec.agent_delta);
         }
       }
       if (rec.job >= 0) {
@@ -82,7 +83,8 @@ __global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t wor
         st.job_partner[rec.job] = rec.job_partner;
         if (rec.job_partner >= 0) {
           const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
-          st.edges[P][pos] = make_int4(n + rec.job, i, rec.job_partner, rec.job);
+          st.edges[P][pos] = job_prop(st.sigma, st.tau, st.A, st.storage, st.ld, n, rec.job, rec.job_partner,
+                                      rec.job_delta);
         }
       }
     }

@@ -152,6 +152,7 @@ __global__ void init_assignment_kernel(DevState d) {
   const E* A = static_cast<const E*>(d.A);
   const int32_t i = d.sigma[j];
   d.tau[i] = j;
+  if (d.tau16) d.tau16[i] = static_cast<uint16_t>(j);
   static_cast<E*>(d.acur)[i] = A[static_cast<int64_t>(i) * d.ld + j];
 }
 

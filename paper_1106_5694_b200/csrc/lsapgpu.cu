@@ -245,6 +245,8 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   d.ld = ld;
   CK(valloc(ctx, &d.sigma, N, true));
   CK(valloc(ctx, &d.tau, N, true));
+  d.tau16 = nullptr;
+  if (n < 65536) CK(valloc(ctx, &d.tau16, N, true));
   void* acur = nullptr;
   CK(valloc(ctx, reinterpret_cast<double**>(&acur), N, true));  // 8 bytes/elem covers any storage
   d.acur = acur;
@@ -252,8 +254,11 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.agent_partner, N, true));
   CK(valloc(ctx, &d.job_delta, N, true));
   CK(valloc(ctx, &d.job_partner, N, true));
-  CK(valloc(ctx, &d.edges[0], N2, false));  // int4 proposal entries
+  CK(valloc(ctx, &d.edges[0], N2, false));  // Prop proposal entries
   CK(valloc(ctx, &d.edges[1], N2, false));
+  CK(valloc(ctx, &d.clist, N, false));
+  CK(valloc(ctx, &d.qlist, N2, false));
+  CK(valloc(ctx, &d.jbits, N / 32 + 1, true));
   CK(valloc(ctx, &d.eu, N2, false));
   CK(valloc(ctx, &d.ev, N2, false));
   CK(valloc(ctx, &d.eprop, N2, false));
@@ -649,6 +654,7 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   if (ctx->flags_dev) cudaFree(ctx->flags_dev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->d.tl) cudaFree(ctx->d.tl);
   if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   if (ctx->stage.p) cudaFree(ctx->stage.p);
   if (ctx->chunk_flags) cudaFree(ctx->chunk_flags);
@@ -776,6 +782,31 @@ int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled) {
   return LSAPGPU_OK;
 }
 
+int lsapgpu_set_timeline(lsapgpu_ctx* ctx, int32_t capacity) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->d.tl) cudaFree(ctx->d.tl);
+  ctx->d.tl = nullptr;
+  ctx->d.tl_cap = 0;
+  if (capacity > 0) {
+    CK(cudaMalloc(&ctx->d.tl, sizeof(unsigned long long) * capacity));
+    ctx->d.tl_cap = capacity;
+  }
+  drop_graph(ctx);  // the graph captured the old DevState
+  return LSAPGPU_OK;
+}
+
+int32_t lsapgpu_timeline(lsapgpu_ctx* ctx, uint64_t* out, int32_t capacity) {
+  if (!ctx || !ctx->d.tl) return 0;
+  if (pull_ctrl(ctx)) return 0;
+  const int32_t cnt = std::min(ctx->ctrl_host->tl_count, std::min(capacity, ctx->d.tl_cap));
+  if (cnt > 0 && cudaMemcpy(out, ctx->d.tl, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  ctx->ctrl_host->tl_count = 0;
+  push_ctrl(ctx);
+  cudaStreamSynchronize(ctx->stream);
+  return cnt;
+}
+
 int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
                         double* full_sweep_ms, int64_t* full_sweeps, double* commit_ms,
                         int64_t* commit_launches) {
@@ -848,12 +879,12 @@ int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_del
   rc = pull_ctrl(ctx);
   if (rc) return rc;
   const int32_t m = ctx->ctrl_host->edge_count[ctx->ctrl_host->parity];
-  std::vector<int4> slots(m);
+  std::vector<Prop> slots(m);
   std::vector<int32_t> eu(m), ev(m);
   std::vector<uint8_t> est(m);
   if (m) {
     const int P = ctx->ctrl_host->parity;
-    CK(cpy(ctx, slots.data(), d.edges[P], sizeof(int4) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cpy(ctx, slots.data(), d.edges[P], sizeof(Prop) * m, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cpy(ctx, eu.data(), d.eu, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cpy(ctx, ev.data(), d.ev, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cpy(ctx, est.data(), d.estate, m, cudaMemcpyDeviceToHost, ctx->stream));
@@ -865,7 +896,7 @@ int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_del
   std::memset(conflicted_mask, 0, n);
   std::vector<int32_t> cj;
   for (int32_t e = 0; e < m; ++e) {
-    const int32_t s = slots[e].x;
+    const int32_t s = slots[e].slot;
     if (est[e] == kEdgeAccepted) {
       (s < n ? agent_accepted[s] : job_accepted[s - n]) = 1;
       reserved_mask[eu[e]] = 1;
@@ -912,6 +943,7 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
   CK(cpy(ctx, masks + n, job_accepted, n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cpy(ctx, d.sigma, sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cpy(ctx, d.tau, tau, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_tau16_sync(d, ctx->stream));
   CK(cpy(ctx, d.agent_delta, ad.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cpy(ctx, d.agent_partner, agent_partner, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cpy(ctx, d.job_delta, jd.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -1089,7 +1121,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       if (multi) {
         for (;;) {
           CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
-          ++ctx->launches;
+          ctx->launches += 2;  // conflict check + apply
           rc = pull_ctrl(ctx);
           if (rc) return rc;
           const Ctrl& C = *ctx->ctrl_host;
@@ -1115,7 +1147,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
             ctx->commit_ms += cms;
             ++ctx->commit_launches;
           }
-          ++ctx->launches;
+          ctx->launches += 2;  // conflict check + apply
           rc = run_scan(ctx, 0);
           if (rc) return rc;
           ++launches;
@@ -1175,9 +1207,10 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.switches_applied = switches;
   const bool graphed = P.use_graph && !multi;
   S.scan_launches = graphed ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
-  // every body pass of the graph is one commit + one scan launch; the last
-  // pass per graph launch finds no active record and exits early
-  if (graphed) ctx->launches += 2 * (S.inner_iterations + graph_launches);
+  // every body pass of the graph is a commit (conflict check + apply) and a
+  // scan launch; the last pass per graph launch finds no active record and
+  // exits early
+  if (graphed) ctx->launches += 3 * (S.inner_iterations + graph_launches);
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 

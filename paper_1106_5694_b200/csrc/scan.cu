@@ -7,7 +7,7 @@
 namespace lsapgpu {
 
 constexpr int kPacked32 = 0, kPacked64 = 1, kFloat = 2;
-constexpr size_t kStaticSmem = 9 * 1024;  // ebuf + item metadata + counters (+ slack)
+constexpr size_t kStaticSmem = 14 * 1024;  // ebuf + item metadata + counters (+ slack)
 
 template <class E, int KM>
 cudaError_t launch_scan_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
@@ -99,8 +99,8 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
   // (LSAPGPU_SCAN_RESIDENT=0 forces the streaming kernel).
   int resident = 1;
   if (const char* r = std::getenv("LSAPGPU_SCAN_RESIDENT")) resident = std::atoi(r);
-  if (resident && d.n < 65536 && !std::getenv("LSAPGPU_SCAN_BUDGET")) {
-    const size_t limit = 227 * 1024 - 6 * 1024;
+  if (resident && d.n < 65536 && d.tau16 && !std::getenv("LSAPGPU_SCAN_BUDGET")) {
+    const size_t limit = 227 * 1024 - 14 * 1024;
     int m = 0;
     for (int mm : {4, 2, 1})
       if (res_smem_bytes(d.ld, es, mm, 2) <= limit) {
@@ -121,6 +121,10 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       p.threads = 512;
       p.smem = res_smem_bytes(d.ld, es, m, bufs);
       p.ctas = num_sms;
+      // splitting items over CTAs re-stages whole rows per segment and adds a
+      // cross-CTA merge; measured slower than whole items at every list size
+      p.max_segments = 1;
+      if (const char* sg = std::getenv("LSAPGPU_SCAN_SEGMENTS")) p.max_segments = std::atoi(sg);
     }
   }
   return p;

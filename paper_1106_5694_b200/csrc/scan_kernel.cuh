@@ -272,7 +272,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Per-CTA emission buffer for active records (EdgeEntry), flushed with one
 // global atomic per flush instead of one dependent atomic per record.
-constexpr int kEdgeBuf = 512;
+constexpr int kEdgeBuf = 256;
 constexpr int kMaxBufs = 4;
 
 template <class E, int M, int NT, int KM, bool kChunked>
@@ -299,11 +299,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
   __shared__ ItemInfo info_s[kMaxBufs][M];
   __shared__ int arrive_cnt[kMaxBufs];
   __shared__ int last_seg;
-  __shared__ int4 ebuf[kEdgeBuf];
+  __shared__ Prop ebuf[kEdgeBuf];
   __shared__ int ebuf_n;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
 
   const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
   if (count <= 0) return;
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
         }
         if (finalize) {
           bool emit = false;
-          int4 entry = make_int4(0, 0, 0, 0);
+          Prop entry;
           if (lane < 2 * M) {
             const ItemInfo im = info_s[b][lane >> 1];
             const bool active = ok && d > st.eps;
@@ -536,13 +537,15 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
                   st.agent_delta[im.agent] = active ? d : 0.0;
                   st.agent_partner[im.agent] = active ? k : -1;
                   emit = active && st.emit_edges;
-                  entry = make_int4(im.agent, im.agent, k, im.job);
+                  if (emit)  // agent i -> job k (entries filled in at the flush)
+                    entry = Prop{im.agent, im.agent, -1, k, im.job, 2, d, 0.0, 0.0};
                 }
               } else if (im.flags & kItemJob) {
                 st.job_delta[im.job] = active ? d : 0.0;
                 st.job_partner[im.job] = active ? k : -1;
                 emit = active && st.emit_edges;
-                entry = make_int4(n + im.job, im.agent, k, im.job);
+                if (emit)  // agent k -> job j0, holder i -> tau[k] (filled in at the flush)
+                  entry = Prop{n + im.job, k, im.agent, im.job, -1, 2, d, 0.0, 0.0};
               }
             }
           }
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
                 ebuf[pos] = entry;
               } else {  // overflow: direct global append
                 const int g = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
-                st.edges[parity_out][g] = entry;
+                st.edges[parity_out][g] = finish_prop(entry, st.sigma, tau, st.A, st.storage, ld, n);
               }
             }
           }
@@ -580,10 +583,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
   __shared__ int gbase;
   if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
   __syncthreads();
-  for (int e = tid; e < ne; e += NT) st.edges[parity_out][gbase + e] = ebuf[e];
+  for (int e = tid; e < ne; e += NT)
+    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau, st.A, st.storage, ld, n);
 }
 
-constexpr size_t kStaticSmem = 9 * 1024;  // ebuf + item metadata + counters (+ slack)
+constexpr size_t kStaticSmem = 14 * 1024;  // ebuf + item metadata + counters (+ slack)
 
 template <class E, int M, int NT, int KM>
 cudaError_t launch_nt(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {

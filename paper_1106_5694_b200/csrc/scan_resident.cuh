@@ -140,11 +140,12 @@ __global__ void __launch_bounds__(kResThreads, 1)
   Track<KM>* red = reinterpret_cast<Track<KM>*>(full_bar + 4 * kMaxBufs);  // [B][NW][2M]
   __shared__ ResInfo info_s[kMaxBufs][M];
   __shared__ int arrive_cnt[kMaxBufs];
-  __shared__ int4 ebuf[kResEdgeBuf];
+  __shared__ Prop ebuf[kResEdgeBuf];
   __shared__ int ebuf_n;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
 
   const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
   if (count <= 0) return;
@@ -185,8 +186,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
 
   if (warp == NW) {
     // ---------------- producer warp ----------------
-    if (lane == 0) {  // resident acur (frozen for the launch)
-      mbar_expect_tx(res_bar, static_cast<uint32_t>(row_bytes));
+    if (lane == 0) {  // resident tau16 and acur (frozen for the launch)
+      const uint32_t tau_bytes = static_cast<uint32_t>((static_cast<size_t>(ld) * 2 + 15) / 16 * 16);
+      mbar_expect_tx(res_bar, tau_bytes + static_cast<uint32_t>(row_bytes));
+      bulk_g2s(tau_s, st.tau16, tau_bytes, res_bar);
       bulk_g2s(acur_s, acur_g, static_cast<uint32_t>(row_bytes), res_bar);
     }
     // Item metadata of the next K stages is kept in flight across the warp:
@@ -261,16 +264,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
     }
   } else {
     // ---------------- consumer warps ----------------
-    // resident tau as uint16 (n < 65536 is a precondition of this kernel)
-    for (int32_t i = tid * 4; i < ld; i += NW * 32 * 4) {
-      const int4 v = __ldg(reinterpret_cast<const int4*>(tau_g + i));
-      uint2 w;
-      w.x = (static_cast<uint32_t>(v.x) & 0xFFFFu) | (static_cast<uint32_t>(v.y) << 16);
-      w.y = (static_cast<uint32_t>(v.z) & 0xFFFFu) | (static_cast<uint32_t>(v.w) << 16);
-      *reinterpret_cast<uint2*>(tau_s + i) = w;
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    // resident tau16 and acur arrive by TMA (n < 65536 is a precondition of this kernel)
     mbar_wait(res_bar, 0);
+    if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 8);
 
     Track<KM> ta[M], tj[M];
     const int32_t nstages = static_cast<int32_t>(stages);
@@ -283,6 +279,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const int32_t seg_lo = seg * seglen;
       const int32_t seg_hi = min(n, seg_lo + seglen);
       mbar_wait_sleep(&full_bar[b], phase);
+      if (q == 0 && blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 9);
       Acc sv[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
@@ -358,21 +355,47 @@ __global__ void __launch_bounds__(kResThreads, 1)
         if (last) arrive_cnt[b] = 0;
       }
       last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
+      if (!last) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[b]);
+      } else {
+        // Last warp of the stage: everything that needs the staged buffer is
+        // read first, the buffer is released, and only then come the global
+        // loads / stores of the finalisation, so the producer can refill the
+        // buffer while they are in flight.
         __threadfence_block();
         Track<KM> r;
         r.init();
         if (lane < 2 * M)
           for (int w = 0; w < NW; ++w) r.merge(rq[w * 2 * M + lane]);
-        bool finalize = (S == 1);
+        const ResInfo im = lane < 2 * M ? info_s[b][lane >> 1] : ResInfo{-1, 0, 0u, 0, 0.0};
+        bool ok = false;
         double d = 0.0;
         int32_t k = -1;
-        bool ok = false;
+        // smem parts of the proposal (S == 1: this CTA finalises the item)
+        int32_t jk = 0;
+        double acur_a = 0.0, acur_d = 0.0;
         if (S == 1) {
-          ok = lane < 2 * M && r.valid();
+          ok = lane < 2 * M && im.agent >= 0 && r.valid();
           d = ok ? r.delta() : 0.0;
           k = ok ? r.index() : -1;
-        } else {
+          if (ok) {
+            const E* rowA = rowsA + static_cast<size_t>(lane >> 1) * ld;
+            const E* rowT = rowsT + static_cast<size_t>(lane >> 1) * ld;
+            if ((lane & 1) == 0) {
+              acur_a = static_cast<double>(rowA[k]);  // A[i][k]
+            } else {
+              jk = tau_s[k];
+              acur_a = static_cast<double>(rowT[k]);   // A[k][j0]
+              acur_d = static_cast<double>(rowA[jk]);  // A[i][tau[k]]
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[b]);
+
+        bool finalize = (S == 1);
+        if (S > 1) {
           // publish this segment's partials; the last segment to arrive combines
           if (lane < 2 * M) {
             const int64_t slot = (static_cast<int64_t>(group) * S + seg) * M + (lane >> 1);
@@ -406,16 +429,24 @@ __global__ void __launch_bounds__(kResThreads, 1)
                 o.i = (lane & 1) ? __ldcg(&st.part_ji[slot]) : __ldcg(&st.part_at[slot]);
                 c.merge(o);
               }
-            ok = lane < 2 * M && c.valid();
+            ok = lane < 2 * M && im.agent >= 0 && c.valid();
             d = c.d;
             k = c.i;
+            if (ok) {  // the staged rows may be gone: read the entries from HBM
+              if ((lane & 1) == 0) {
+                acur_a = static_cast<double>(A[static_cast<int64_t>(im.agent) * ld + k]);
+              } else {
+                jk = tau_g[k];
+                acur_a = static_cast<double>(AT[static_cast<int64_t>(im.job) * ld + k]);
+                acur_d = static_cast<double>(A[static_cast<int64_t>(im.agent) * ld + jk]);
+              }
+            }
           }
         }
         if (finalize) {
           bool emit = false;
-          int4 entry = make_int4(0, 0, 0, 0);
+          Prop entry;
           if (lane < 2 * M) {
-            const ResInfo im = info_s[b][lane >> 1];
             const bool active = ok && d > st.eps;
             if (im.agent >= 0) {
               if ((lane & 1) == 0) {
@@ -423,13 +454,15 @@ __global__ void __launch_bounds__(kResThreads, 1)
                   st.agent_delta[im.agent] = active ? d : 0.0;
                   st.agent_partner[im.agent] = active ? k : -1;
                   emit = active && st.emit_edges;
-                  entry = make_int4(im.agent, im.agent, k, im.job);
+                  if (emit)  // agent i -> job k; displaced holder filled in at the flush
+                    entry = Prop{im.agent, im.agent, -1, k, im.job, 1, d, acur_a, 0.0};
                 }
               } else if (im.flags & kItemJob) {
                 st.job_delta[im.job] = active ? d : 0.0;
                 st.job_partner[im.job] = active ? k : -1;
                 emit = active && st.emit_edges;
-                entry = make_int4(n + im.job, im.agent, k, im.job);
+                if (emit)  // agent k -> job j0, holder i -> tau[k]
+                  entry = Prop{n + im.job, k, im.agent, im.job, jk, 0, d, acur_a, acur_d};
               }
             }
           }
@@ -444,14 +477,12 @@ __global__ void __launch_bounds__(kResThreads, 1)
                 ebuf[pos] = entry;
               } else {  // overflow: direct global append
                 const int g = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
-                st.edges[parity_out][g] = entry;
+                st.edges[parity_out][g] = finish_prop(entry, st.sigma, tau_g, st.A, st.storage, ld, n);
               }
             }
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[b]);
       if (++b == bufs) {
         b = 0;
         phase ^= 1u;
@@ -460,11 +491,13 @@ __global__ void __launch_bounds__(kResThreads, 1)
   }
   // flush the CTA's buffered edges
   __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 10);
   const int ne = min(ebuf_n, kResEdgeBuf);
   __shared__ int gbase;
   if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
   __syncthreads();
-  for (int e = tid; e < ne; e += kResThreads) st.edges[parity_out][gbase + e] = ebuf[e];
+  for (int e = tid; e < ne; e += kResThreads)
+    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.A, st.storage, ld, n);
 }
 
 // Dynamic smem of the resident kernel for (ld, elem size, M, bufs).

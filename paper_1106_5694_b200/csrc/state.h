@@ -23,6 +23,7 @@ struct DevState {
   const void* AT = nullptr;  // transposed, n x ld
   int32_t* sigma = nullptr;  // job -> agent (padded to ld)
   int32_t* tau = nullptr;    // agent -> job (padded to ld)
+  uint16_t* tau16 = nullptr; // the same as uint16 when n < 65536 (the resident scan bulk-loads it)
   void* acur = nullptr;      // A[i][tau[i]] (storage type, padded to ld)
 
   double* agent_delta = nullptr;
@@ -30,10 +31,13 @@ struct DevState {
   double* job_delta = nullptr;
   int32_t* job_partner = nullptr;
 
-  // active proposals, capacity 2n each: {slot, a, b, c} with slot = i (agent
-  // record of i: a = i, b = partner job, c = tau[i]) or n + j (job record of j:
-  // a = sigma[j], b = partner agent, c = j), written by the pair scan
-  int4* edges[2] = {nullptr, nullptr};
+  // active proposals (Prop, common.cuh), capacity 2n each, ping-pong
+  Prop* edges[2] = {nullptr, nullptr};
+  // split commit: committed / queued-conflicted proposal indices and the
+  // rejected-job bitmap of the batch (commit_single.cuh -> commit_apply)
+  int32_t* clist = nullptr;
+  int32_t* qlist = nullptr;
+  uint32_t* jbits = nullptr;
   int32_t* eu = nullptr;                   // LFMM scratch: endpoint u, capacity 2n
   int32_t* ev = nullptr;                   // endpoint v
   int32_t* eprop = nullptr;                // proposer agent (frozen sigma)
@@ -68,6 +72,10 @@ struct DevState {
   uint32_t* items_own = nullptr;
   int use_own = 0;
   int emit_edges = 1;
+  // device timeline (instrumentation): CTA 0 of every scan / commit launch
+  // appends (%globaltimer << 4 | kind); null when disabled
+  unsigned long long* tl = nullptr;
+  int tl_cap = 0;
 };
 
 // ---- launchers (implemented in the .cu files) -------------------------------
@@ -125,6 +133,7 @@ struct CommitPlan {
   int cluster = 8;          // cluster kernel: CTAs per cluster (16 or 8)
   size_t cluster_smem = 0;  // cluster kernel: dynamic smem per CTA
   int edge_cap = 0;         // cluster kernel: proposals per CTA held in smem
+  int cta_edge_cap = 0;     // single-CTA path taken when the proposals fit one CTA (0: never)
 };
 CommitPlan plan_commit(const DevState& d);
 cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
@@ -134,6 +143,7 @@ cudaError_t launch_commit_cluster(const DevState& d, const CommitPlan& p, int mo
                                   cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st);
 // step-API helpers
 cudaError_t launch_edges_from_tables(const DevState& d, cudaStream_t st);
+cudaError_t launch_tau16_sync(const DevState& d, cudaStream_t st);
 cudaError_t launch_accepted_from_masks(const DevState& d, const uint8_t* agent_acc,
                                        const uint8_t* job_acc, cudaStream_t st);
 

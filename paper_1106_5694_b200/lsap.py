@@ -447,6 +447,16 @@ class Context:
     def stream(self) -> int:
         return int(N.LIB.lsapgpu_stream(self.h) or 0)
 
+    def set_timeline(self, capacity: int) -> None:
+        """Enable (capacity > 0) or disable the device timeline of scan / commit launches."""
+        self._check(N.LIB.lsapgpu_set_timeline(self.h, int(capacity)))
+
+    def timeline(self, capacity: int = 4096):
+        """[(t_ns, kind)] since the last call; kind 1 full sweep, 2 scan, 3 commit, 4 commit end."""
+        buf = np.zeros(capacity, np.uint64)
+        cnt = N.LIB.lsapgpu_timeline(self.h, buf.ctypes.data, capacity)
+        return [(int(v >> 4), int(v & 15)) for v in buf[:cnt]]
+
     def set_scan_timing(self, on: bool) -> None:
         self._check(N.LIB.lsapgpu_set_scan_timing(self.h, 1 if on else 0))
 
