@@ -152,6 +152,8 @@ __global__ void __launch_bounds__(1024, 1)
 template <class E>
 __global__ void __launch_bounds__(256) commit_apply_kernel(DevState st) {
   Ctrl* C = st.ctrl;
+  pdl_trigger();
+  pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark(C, st.tl, st.tl_cap, 15);
   const int32_t nlog = C->k2_nlog, nconf = C->k2_nconf;
   if (nlog + nconf == 0) return;
@@ -203,13 +205,12 @@ __global__ void __launch_bounds__(256) commit_apply_kernel(DevState st) {
 
 cudaError_t launch_commit_apply(const DevState& d, cudaStream_t st) {
   switch (d.storage) {
-    case kI16: commit_apply_kernel<int16_t><<<64, 256, 0, st>>>(d); break;
-    case kI32: commit_apply_kernel<int32_t><<<64, 256, 0, st>>>(d); break;
-    case kF32: commit_apply_kernel<float><<<64, 256, 0, st>>>(d); break;
-    case kF64: commit_apply_kernel<double><<<64, 256, 0, st>>>(d); break;
+    case kI16: return launch_pdl(commit_apply_kernel<int16_t>, dim3(64), dim3(256), 0, st, d.pdl, d);
+    case kI32: return launch_pdl(commit_apply_kernel<int32_t>, dim3(64), dim3(256), 0, st, d.pdl, d);
+    case kF32: return launch_pdl(commit_apply_kernel<float>, dim3(64), dim3(256), 0, st, d.pdl, d);
+    case kF64: return launch_pdl(commit_apply_kernel<double>, dim3(64), dim3(256), 0, st, d.pdl, d);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 CommitPlan plan_commit(const DevState& d) {

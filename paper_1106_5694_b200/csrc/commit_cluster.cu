@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(kNT, 1)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CommitScratch sc;
   __shared__ uint32_t* kbase[CS];
@@ -407,13 +409,15 @@ cudaError_t launch_cs(const DevState& d, const CommitPlan& p, int mode, cudaGrap
   cfg.blockDim = dim3(kNT);
   cfg.dynamicSmemBytes = p.cluster_smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = d.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap);
 }
 

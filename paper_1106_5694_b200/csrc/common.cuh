@@ -186,12 +186,38 @@ __device__ __forceinline__ Prop finish_prop(Prop p, const int32_t* sigma, const 
   return p;
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor drains; it must wait for the
+// predecessor's completion (and memory) before touching state the
+// predecessor writes.  Both are no-ops for a normally launched kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // timeline kinds
 constexpr unsigned kTlScanFull = 1, kTlScan = 2, kTlCommit = 3, kTlCommitEnd = 4;
 __device__ __forceinline__ void tl_mark(Ctrl* c, unsigned long long* tl, int cap, unsigned kind) {
   if (tl == nullptr) return;
   const int i = atomicAdd(&c->tl_count, 1);
   if (i < cap) tl[i] = (globaltimer() << 4) | kind;
+}
+
+// Launch helper: cudaLaunchKernelEx with programmatic stream serialization
+// when enabled (pdl != 0), so consecutive kernels of the inner loop overlap
+// one's tail with the next one's launch.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int pdl,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 }  // namespace lsapgpu

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -619,6 +620,8 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
     return LSAPGPU_ERR_CUDA;
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  ctx->d.pdl = 1;  // programmatic dependent launch for the inner-loop kernels (LSAPGPU_PDL=0: off)
+  if (const char* e = std::getenv("LSAPGPU_PDL")) ctx->d.pdl = std::atoi(e) != 0;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||

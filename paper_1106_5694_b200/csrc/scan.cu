@@ -16,7 +16,7 @@ cudaError_t launch_scan_res_typed(const DevState& d, const ScanPlan& p, int full
 
 // Resident-state kernel geometry (scan_resident.cuh): 15 consumer warps + 1
 // producer, tau16 + acur resident, double-buffered (A row, AT row) stages.
-constexpr int kResWarps = 15;
+constexpr int kResWarps = 23;  // reduction scratch sized for the widest resident CTA
 constexpr int kMaxBufs = 4;
 size_t res_smem_bytes(int64_t ld, size_t es, int M, int bufs) {
   const size_t row = static_cast<size_t>(ld) * es;
@@ -119,12 +119,16 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       p.passes = 1;
       p.chunk = d.ld;
       p.threads = 512;
+      if (const char* t = std::getenv("LSAPGPU_SCAN_RES_NT")) p.threads = std::atoi(t);
       p.smem = res_smem_bytes(d.ld, es, m, bufs);
       p.ctas = num_sms;
       // splitting items over CTAs re-stages whole rows per segment and adds a
       // cross-CTA merge; measured slower than whole items at every list size
       p.max_segments = 1;
       if (const char* sg = std::getenv("LSAPGPU_SCAN_SEGMENTS")) p.max_segments = std::atoi(sg);
+      p.l2_prefetch = 0;  // measured slower at every distance (tools/ab.py)
+      if (const char* pf = std::getenv("LSAPGPU_SCAN_L2PF")) p.l2_prefetch = std::atoi(pf);
+      if (p.l2_prefetch >= 32 / m) p.l2_prefetch = 32 / m - 1;
     }
   }
   return p;

@@ -304,6 +304,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();
+  pdl_wait();
   if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
 
   const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
@@ -595,8 +597,8 @@ cudaError_t launch_nt(const DevState& d, const ScanPlan& p, int full, cudaStream
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;
-  k<<<p.ctas, NT, p.smem, st>>>(d, full, p.passes, p.chunk, p.bufs, p.max_segments);
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(p.ctas), dim3(NT), p.smem, st, d.pdl, d, full, p.passes, p.chunk, p.bufs,
+                    p.max_segments);
 }
 
 template <class E, int M, int KM>

@@ -25,8 +25,7 @@
 namespace lsapgpu {
 namespace scan_detail {
 
-constexpr int kResThreads = 512;            // 15 consumer warps + 1 producer warp
-constexpr int kResWarps = kResThreads / 32 - 1;
+constexpr int kResMaxWarps = 23;  // consumer warps at most (reduction scratch sizing)
 constexpr int kResEdgeBuf = 256;
 
 struct ResInfo {
@@ -110,14 +109,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // smem: tau16[ld] | acur[ld] | stages [bufs][2][M][ld] (A rows, AT rows) |
 //       full[4], empty[4], res[1] mbarriers | red[bufs][NW][2M]
-template <class E, int M, int KM>
+template <class E, int M, int KM, int kResThreads>
 __global__ void __launch_bounds__(kResThreads, 1)
-    pair_scan_res_kernel(DevState st, int full, int bufs, int max_segments) {
+    pair_scan_res_kernel(DevState st, int full, int bufs, int max_segments, int pf) {
   using Acc = typename Traits<E>::Acc;
   constexpr int V = 16 / sizeof(E);
-  constexpr int NW = kResWarps;
+  constexpr int NW = kResThreads / 32 - 1;  // consumer warps; the last warp produces
   constexpr int32_t kBlk = 32 * V;
   constexpr int32_t kStride = NW * kBlk;
 
@@ -145,6 +148,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();  // persistent single-wave grid: the next kernel may queue now
+  pdl_wait();     // the commit / apply before this scan wrote the state it reads
   if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
 
   const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
@@ -226,6 +231,13 @@ __global__ void __launch_bounds__(kResThreads, 1)
       cur.pad = 0;
       cur.sv = 0.0;
       if (lane / M == static_cast<int>(q % K)) mine = load_info(q + K);  // refill this slot
+      // Warm L2 with the rows of stage q + pf: the HBM stream then runs pf
+      // stages ahead of the two shared-memory buffers, and the TMA copies of
+      // a released buffer are served from L2.
+      if (pf > 0 && lane / M == static_cast<int>((q + pf) % K) && q + pf < stages && mine.agent >= 0) {
+        l2_prefetch(A + static_cast<int64_t>(mine.agent) * ld, static_cast<uint32_t>(row_bytes));
+        l2_prefetch(AT + static_cast<int64_t>(mine.job) * ld, static_cast<uint32_t>(row_bytes));
+      }
       if (q >= bufs) mbar_wait(&empty_bar[b], static_cast<uint32_t>(((q / bufs) - 1) & 1));
       if (lane < M) info_s[b][lane] = cur;
       __syncwarp();
@@ -235,6 +247,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
 #pragma unroll
         for (int m = 0; m < M; ++m)
           if (info_s[b][m].agent >= 0) total += 2u * static_cast<uint32_t>(row_bytes);
+        if (pf == -3) {  // timing probe only: the scan on stale stage data, no row traffic
+          mbar_arrive(&full_bar[b]);
+        } else {
         mbar_expect_tx(&full_bar[b], total);
         unsigned char* sb = stage_base + b * stage_bytes;
         // full sweeps stage M consecutive agents: their A rows are one
@@ -259,6 +274,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                    reinterpret_cast<const unsigned char*>(AT + static_cast<int64_t>(im.job) * ld),
                    static_cast<uint32_t>(row_bytes), &full_bar[b]);
         }
+        }
       }
       __syncwarp();
     }
@@ -273,12 +289,20 @@ __global__ void __launch_bounds__(kResThreads, 1)
     int b = 0;
     uint32_t phase = 0;
     int32_t uq = blockIdx.x;
+    int32_t rot = 0;
     for (int32_t q = 0; q < nstages; ++q, uq += gridDim.x) {
-      const int32_t group = uq / S;
+      const int32_t group = S == 1 ? uq : uq / S;
       const int32_t seg = uq - group * S;
       const int32_t seg_lo = seg * seglen;
       const int32_t seg_hi = min(n, seg_lo + seglen);
-      mbar_wait_sleep(&full_bar[b], phase);
+      // A stage has ceil(len / kBlk) blocks for NW warps; the warp that takes
+      // block 0 rotates from stage to stage so the warps that get one block
+      // more than the others change every stage and no warp falls behind
+      // (a buffer is released only when its slowest warp is done).
+      const int32_t nblk = (seg_hi - seg_lo + kBlk - 1) / kBlk;
+      const int32_t wslot = (warp + NW - rot) % NW;
+      rot = (rot + nblk) % NW;
+      if (pf == -2) mbar_wait_sleep(&full_bar[b], phase); else mbar_wait(&full_bar[b], phase);
       if (q == 0 && blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 9);
       Acc sv[M];
 #pragma unroll
@@ -291,7 +315,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const E* rowsA = reinterpret_cast<const E*>(stage_base + b * stage_bytes);
       const E* rowsT = rowsA + static_cast<size_t>(M) * ld;
 
-      if constexpr (KM == kPacked32) {
+      if (pf == -1) {
+        // timing probe only (LSAPGPU_SCAN_L2PF = -1): data movement without the scan
+      } else if constexpr (KM == kPacked32) {
         uint32_t ka[M], kj[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -299,7 +325,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
           kj[m] = 0u;
         }
         const uint32_t pitch_b = static_cast<uint32_t>(row_bytes);
-        int32_t i0 = seg_lo + warp * kBlk + lane * V;
+        int32_t i0 = seg_lo + wslot * kBlk + lane * V;
         for (; i0 + V <= seg_hi; i0 += kStride) {
           const uint4 tw = *reinterpret_cast<const uint4*>(tau_s + i0);
           const uint4 cw = *reinterpret_cast<const uint4*>(acur_s + i0);
@@ -324,7 +350,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
           compute_step<E, M, KM, false>(r, i0, seg_hi - i0, rowsA, ld, 0, sv, ta, tj);
         }
       } else {
-        for (int32_t i0 = seg_lo + warp * kBlk + lane * V; i0 < seg_hi; i0 += kStride) {
+        for (int32_t i0 = seg_lo + wslot * kBlk + lane * V; i0 < seg_hi; i0 += kStride) {
           StreamRegs<E, M> r;
           lds_tau<E>(tau_s + i0, r.t);
           r.c = *reinterpret_cast<const uint4*>(acur_s + i0);
@@ -498,6 +524,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
   __syncthreads();
   for (int e = tid; e < ne; e += kResThreads)
     st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.A, st.storage, ld, n);
+  if (st.tl_cap > 8192) {  // per-CTA end stamps (deep instrumentation only)
+    __syncthreads();
+    if (tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, stages > 1 ? 12 : 11);
+  }
 }
 
 // Dynamic smem of the resident kernel for (ld, elem size, M, bufs).
@@ -506,17 +536,26 @@ inline size_t res_smem_bytes(int64_t ld, size_t es, int M, int bufs) {
   const size_t tau = (static_cast<size_t>(ld) * 2 + 127) / 128 * 128;
   const size_t acur = (row + 127) / 128 * 128;
   return tau + acur + static_cast<size_t>(bufs) * 2 * M * row + 4 * kMaxBufs * 8 +
-         static_cast<size_t>(bufs) * kResWarps * 2 * M * 16;
+         static_cast<size_t>(bufs) * kResMaxWarps * 2 * M * 16;
+}
+
+template <class E, int M, int KM, int NTR>
+cudaError_t launch_res_t(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  auto k = pair_scan_res_kernel<E, M, KM, NTR>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(p.smem));
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k, dim3(p.ctas), dim3(NTR), p.smem, st, d.pdl, d, full, p.bufs, p.max_segments,
+                    p.l2_prefetch);
 }
 
 template <class E, int M, int KM>
 cudaError_t launch_res_m(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  auto k = pair_scan_res_kernel<E, M, KM>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(p.smem));
-  if (e != cudaSuccess) return e;
-  k<<<p.ctas, kResThreads, p.smem, st>>>(d, full, p.bufs, p.max_segments);
-  return cudaGetLastError();
+  switch (p.threads) {
+    case 640: return launch_res_t<E, M, KM, 640>(d, p, full, st);
+    case 768: return launch_res_t<E, M, KM, 768>(d, p, full, st);
+    default: return launch_res_t<E, M, KM, 512>(d, p, full, st);
+  }
 }
 
 template <class E, int KM>

@@ -72,6 +72,7 @@ struct DevState {
   uint32_t* items_own = nullptr;
   int use_own = 0;
   int emit_edges = 1;
+  int pdl = 0;  // launch the inner-loop kernels with programmatic dependent launch
   // device timeline (instrumentation): CTA 0 of every scan / commit launch
   // appends (%globaltimer << 4 | kind); null when disabled
   unsigned long long* tl = nullptr;
@@ -112,6 +113,7 @@ struct ScanPlan {
   size_t smem = 0;      // dynamic smem per CTA
   int max_segments = 1;
   int resident = 0;     // 1: resident-state kernel (scan_resident.cuh)
+  int l2_prefetch = 0;  // resident kernel: stages whose rows are prefetched into L2 ahead
 };
 ScanPlan plan_scan(const DevState& d, int num_sms);
 // full sweep (identity work list, count n) when full != 0, else the device work list
