@@ -224,9 +224,9 @@ CommitPlan plan_commit(const DevState& d) {
   p.edge_cap = static_cast<int>(cap / 16 * 16);
   // split commit (commit_single.cuh): per-agent keys + rejected-job bitmap,
   // 13 B per proposal, in one CTA's shared memory
-  // One SM's load/store throughput makes the split commit slower than the
-  // cluster for the large early batches; it wins below a few thousand
-  // proposals (measured on B200, C2/C3: 2k-6k best).
+  // One SM's atomic and load/store throughput makes the split commit slower
+  // than the cluster for the large early batches; it wins below a few
+  // thousand proposals (measured on B200, C2/C3: 2k-6k best).
   p.cta_edge_cap = std::min(single::edge_capacity(d.n, budget), 4096);
   if (p.cta_edge_cap < 1024) p.cta_edge_cap = 0;
   if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE"))

@@ -46,6 +46,7 @@ constexpr int kNT = 1024;
 constexpr uint32_t kTouched = 1u, kQueued = 2u, kJobRejected = 4u;
 constexpr int32_t kNoEmit = -1;
 constexpr int32_t kJobFlagBit = 1 << 30;
+constexpr int32_t kSingleLoad = 2048;  // proposals rank 0 of the split commit loads alone
 
 __device__ __forceinline__ uint32_t make_key(uint32_t round, int32_t slot) {
   return (round << kKeyShift) | (0x3FFFFu - static_cast<uint32_t>(slot));
@@ -122,7 +123,16 @@ __global__ void __launch_bounds__(kNT, 1)
   // and the scattered writes follow grid-wide in commit_apply_kernel
   // (commit_single.cuh).  Otherwise the whole cluster runs the iteration.
   if (m <= cta_cap && (st.policy == 0 || mode == kCommitCheckOnly)) {
-    if (rank == 0) single::commit_single(st, mode, cta_cap, smem);
+    if (m <= kSingleLoad) {  // few proposals: rank 0 loads them itself
+      if (rank == 0) single::commit_single(st, mode, cta_cap, smem);
+      return;
+    }
+    // many: every rank loads a share straight into rank 0's shared memory
+    unsigned char* dst = cluster.map_shared_rank(smem, 0);
+    const int32_t per = (m + CS - 1) / CS;
+    single::load_share(st, cta_cap, dst, min(m, rank * per), min(m, (rank + 1) * per));
+    cluster.sync();
+    if (rank == 0) single::commit_single(st, mode, cta_cap, smem, true);
     return;
   }
   const int32_t iter = C->iter + 1;
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(kNT, 1)
       const int32_t u = Ea.u[l], v = Ea.v[l];
       uint32_t* ku = kbase[u % CS] + u / CS;
       uint32_t* kv = kbase[v % CS] + v / CS;
-      if (*ku == kMatched || *kv == kMatched) {
+      if (rounds > 0 && (*ku == kMatched || *kv == kMatched)) {  // nothing is matched in round 1
         Ea.st[l] = kEdgeRejected;
       } else {
         const uint32_t k = make_key(R, Ea.slot[l]);

@@ -59,7 +59,12 @@ __host__ __device__ inline int edge_capacity(int32_t n, size_t smem) {
 // proposal indices, the rejected-job bitmap and the batch counters for
 // commit_apply_kernel; under kCommitCheckOnly writes the step API's
 // per-proposal state instead.
-__device__ __forceinline__ void commit_single(const DevState& st, int mode, int edge_cap, unsigned char* smem) {
+//
+// Loading the proposals: with `preloaded` the cluster has already written
+// slot / a / d / state of every proposal into this CTA's shared memory
+// (load_share below), otherwise the CTA loads them itself.
+__device__ __forceinline__ void commit_single(const DevState& st, int mode, int edge_cap, unsigned char* smem,
+                                              bool preloaded = false) {
   const int tid = threadIdx.x;
   __shared__ Scratch sc;
 
@@ -80,13 +85,14 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
   if (tid == 0) sc.nlog = sc.nconf = 0;
   for (int32_t x = tid; x < n; x += kNT) keys[x] = 0u;
   for (int32_t x = tid; x < (n + 31) / 32; x += kNT) jbits[x] = 0u;
-  for (int32_t l = tid; l < m; l += kNT) {
-    const int4 h = *reinterpret_cast<const int4*>(&edges[l]);  // slot, a, d, j_new
-    Eslot[l] = h.x;
-    Ea[l] = static_cast<uint16_t>(h.y);
-    Ed[l] = static_cast<uint16_t>(h.z);
-    Est[l] = kEdgeUndecided;
-  }
+  if (!preloaded)
+    for (int32_t l = tid; l < m; l += kNT) {
+      const int4 h = *reinterpret_cast<const int4*>(&edges[l]);  // slot, a, d, j_new
+      Eslot[l] = h.x;
+      Ea[l] = static_cast<uint16_t>(h.y);
+      Ed[l] = static_cast<uint16_t>(h.z);
+      Est[l] = kEdgeUndecided;
+    }
   __syncthreads();
   if (tid == 0) tl_mark(C, st.tl, st.tl_cap, 5);
 
@@ -142,11 +148,20 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
   }
 
   // ---- classify: committed (= accepted, see header) and rejected ----
-  for (int32_t l = tid; l < m; l += kNT) {
-    const uint8_t s = Est[l];
-    if (s == kEdgeAccepted) {
-      st.clist[atomicAdd(&sc.nlog, 1)] = l;
-    } else if (s == kEdgeRejected && Eslot[l] >= n) {
+  // (list appends are warp-aggregated: one shared atomic per warp and pass)
+  const int lane = tid & 31;
+  for (int32_t base = tid - lane; base < m; base += kNT) {
+    const int32_t l = base + lane;
+    const uint8_t s = l < m ? Est[l] : kEdgeUndecided;
+    const bool acc = s == kEdgeAccepted;
+    const unsigned am = __ballot_sync(0xffffffffu, acc);
+    if (am) {
+      int r0 = 0;
+      if (lane == 0) r0 = atomicAdd(&sc.nlog, __popc(am));
+      r0 = __shfl_sync(0xffffffffu, r0, 0);
+      if (acc) st.clist[r0 + __popc(am & ((1u << lane) - 1))] = l;
+    }
+    if (s == kEdgeRejected && Eslot[l] >= n) {
       const int32_t j = Eslot[l] - n;
       atomicOr(&jbits[j >> 5], 1u << (j & 31));
     }
@@ -154,11 +169,20 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
   __syncthreads();
   // conflicted proposers: untouched (unmatched) owners of rejected records,
   // each queued once (the reference's `conflicted` set, parallel.cpp:312-330)
-  for (int32_t l = tid; l < m; l += kNT) {
-    if (Est[l] != kEdgeRejected) continue;
-    const int32_t p = Eslot[l] < n ? Ea[l] : Ed[l];
-    if (keys[p] == kMatched) continue;
-    if (atomicExch(&keys[p], kQueued) != kQueued) st.qlist[atomicAdd(&sc.nconf, 1)] = l;
+  for (int32_t base = tid - lane; base < m; base += kNT) {
+    const int32_t l = base + lane;
+    bool q = false;
+    if (l < m && Est[l] == kEdgeRejected) {
+      const int32_t p = Eslot[l] < n ? Ea[l] : Ed[l];
+      q = keys[p] != kMatched && atomicExch(&keys[p], kQueued) != kQueued;
+    }
+    const unsigned qm = __ballot_sync(0xffffffffu, q);
+    if (qm) {
+      int r0 = 0;
+      if (lane == 0) r0 = atomicAdd(&sc.nconf, __popc(qm));
+      r0 = __shfl_sync(0xffffffffu, r0, 0);
+      if (q) st.qlist[r0 + __popc(qm & ((1u << lane) - 1))] = l;
+    }
   }
   for (int32_t x = tid; x < (n + 31) / 32; x += kNT) st.jbits[x] = jbits[x];
   __syncthreads();
@@ -183,6 +207,26 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
     // anytime deadline, acted on by the next commit (solver_state.hpp:13-27)
     if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
     tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
+  }
+}
+
+// One cluster CTA's share of the proposal load for a preloaded
+// commit_single: proposals [l0, l1) written straight into the shared memory
+// of the CTA that runs the conflict check (`dst` = its mapped smem base).
+__device__ __forceinline__ void load_share(const DevState& st, int edge_cap, unsigned char* dst, int32_t l0,
+                                           int32_t l1) {
+  const int32_t n = st.n;
+  const Prop* edges = st.edges[st.ctrl->parity];
+  int32_t* Eslot = reinterpret_cast<int32_t*>(dst + keys_bytes(n) + jbits_bytes(n));
+  uint16_t* Ea = reinterpret_cast<uint16_t*>(Eslot + edge_cap);
+  uint16_t* Ed = Ea + edge_cap;
+  uint8_t* Est = reinterpret_cast<uint8_t*>(Ed + edge_cap);
+  for (int32_t l = l0 + static_cast<int32_t>(threadIdx.x); l < l1; l += kNT) {
+    const int4 h = *reinterpret_cast<const int4*>(&edges[l]);  // slot, a, d, j_new
+    Eslot[l] = h.x;
+    Ea[l] = static_cast<uint16_t>(h.y);
+    Ed[l] = static_cast<uint16_t>(h.z);
+    Est[l] = kEdgeUndecided;
   }
 }
 

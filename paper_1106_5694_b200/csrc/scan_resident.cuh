@@ -91,11 +91,29 @@ __device__ __forceinline__ void res_step_p32(const uint4& tw, const uint4& cw, c
       const uint32_t xword = (&xw[m].x)[h >> 1];
       const int32_t x = (h & 1) ? (static_cast<int32_t>(xword) >> 16)
                                 : static_cast<int32_t>(static_cast<int16_t>(xword & 0xFFFFu));
-      const uint32_t f = static_cast<uint32_t>(g + x);
-      ka[m] = max(ka[m], f * 16384u + pa);
-      kj[m] = max(kj[m], f * 16384u + pj);
+      const uint32_t fs = static_cast<uint32_t>(g + x) << 14;  // one shift, two fused add-max
+      ka[m] = max(ka[m], fs + pa);
+      kj[m] = max(kj[m], fs + pj);
     }
   }
+}
+
+// mbarrier wait with nanosleep back-off: a warp that finds its stage not
+// ready yet stops competing for issue slots with the warps still computing
+// (a plain try_wait loop spent ~17% of the scan's issued instructions).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
 }
 
 // mbarrier wait that suspends the warp between polls instead of spinning
@@ -143,6 +161,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
   Track<KM>* red = reinterpret_cast<Track<KM>*>(full_bar + 4 * kMaxBufs);  // [B][NW][2M]
   __shared__ ResInfo info_s[kMaxBufs][M];
   __shared__ int arrive_cnt[kMaxBufs];
+  __shared__ int blk_next[kMaxBufs];  // next unclaimed position block of the stage in buffer b
   __shared__ Prop ebuf[kResEdgeBuf];
   __shared__ int ebuf_n;
 
@@ -220,26 +239,35 @@ __global__ void __launch_bounds__(kResThreads, 1)
       }
       return it;
     };
-    ResInfo mine = load_info(lane / M);
+    // Two registers per lane: `mine` is what the shuffles read, `next` has
+    // the loads in flight.  A lane promotes next -> mine only in the
+    // iteration its slot is consumed (K stages after the loads were issued),
+    // so no shuffle ever waits on an outstanding load.
+    ResInfo next = load_info(lane / M);
+    ResInfo mine = next;
     for (int64_t q = 0; q < stages; ++q) {
       const int b = static_cast<int>(q % bufs);
       const int src = static_cast<int>(q % K) * M + (lane % M);
+      const bool owner = lane / M == static_cast<int>(q % K);
+      if (owner) mine = next;
       ResInfo cur;
       cur.agent = __shfl_sync(0xffffffffu, mine.agent, src);
       cur.job = __shfl_sync(0xffffffffu, mine.job, src);
       cur.flags = __shfl_sync(0xffffffffu, mine.flags, src);
       cur.pad = 0;
       cur.sv = 0.0;
-      if (lane / M == static_cast<int>(q % K)) mine = load_info(q + K);  // refill this slot
+      if (owner) next = load_info(q + K);  // refill this slot
       // Warm L2 with the rows of stage q + pf: the HBM stream then runs pf
       // stages ahead of the two shared-memory buffers, and the TMA copies of
       // a released buffer are served from L2.
-      if (pf > 0 && lane / M == static_cast<int>((q + pf) % K) && q + pf < stages && mine.agent >= 0) {
-        l2_prefetch(A + static_cast<int64_t>(mine.agent) * ld, static_cast<uint32_t>(row_bytes));
-        l2_prefetch(AT + static_cast<int64_t>(mine.job) * ld, static_cast<uint32_t>(row_bytes));
+      if (pf > 0 && lane / M == static_cast<int>((q + pf) % K) && q + pf < stages && next.agent >= 0) {
+        l2_prefetch(A + static_cast<int64_t>(next.agent) * ld, static_cast<uint32_t>(row_bytes));
+        l2_prefetch(AT + static_cast<int64_t>(next.job) * ld, static_cast<uint32_t>(row_bytes));
       }
-      if (q >= bufs) mbar_wait(&empty_bar[b], static_cast<uint32_t>(((q / bufs) - 1) & 1));
+      if (q >= bufs) mbar_wait_backoff(&empty_bar[b], static_cast<uint32_t>(((q / bufs) - 1) & 1), 32);
+      if (st.tl_cap > 8192 && blockIdx.x == 0 && lane == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 13);
       if (lane < M) info_s[b][lane] = cur;
+      if (lane == 0) blk_next[b] = 0;
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
@@ -289,21 +317,26 @@ __global__ void __launch_bounds__(kResThreads, 1)
     int b = 0;
     uint32_t phase = 0;
     int32_t uq = blockIdx.x;
-    int32_t rot = 0;
     for (int32_t q = 0; q < nstages; ++q, uq += gridDim.x) {
       const int32_t group = S == 1 ? uq : uq / S;
       const int32_t seg = uq - group * S;
       const int32_t seg_lo = seg * seglen;
       const int32_t seg_hi = min(n, seg_lo + seglen);
-      // A stage has ceil(len / kBlk) blocks for NW warps; the warp that takes
-      // block 0 rotates from stage to stage so the warps that get one block
-      // more than the others change every stage and no warp falls behind
-      // (a buffer is released only when its slowest warp is done).
+      // Position blocks (32 lanes x V) are claimed dynamically from a per-buffer
+      // counter: a warp that finishes its previous stage early takes more
+      // blocks of this one, so all warps stay busy and a buffer is released
+      // soon after its last block is done (static assignment left the warps
+      // with one extra block idling ~1 block per stage behind the slowest).
       const int32_t nblk = (seg_hi - seg_lo + kBlk - 1) / kBlk;
-      const int32_t wslot = (warp + NW - rot) % NW;
-      rot = (rot + nblk) % NW;
-      if (pf == -2) mbar_wait_sleep(&full_bar[b], phase); else mbar_wait(&full_bar[b], phase);
+      auto grab = [&]() -> int32_t {
+        int32_t k = 0;
+        if (lane == 0) k = atomicAdd(&blk_next[b], 1);
+        return __shfl_sync(0xffffffffu, k, 0);
+      };
+      mbar_wait_backoff(&full_bar[b], phase, 64);
       if (q == 0 && blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 9);
+      if (st.tl_cap > 8192 && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == NW - 1))
+        tl_mark(st.ctrl, st.tl, st.tl_cap, warp == 0 ? 11 : 14);
       Acc sv[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
@@ -325,14 +358,22 @@ __global__ void __launch_bounds__(kResThreads, 1)
           kj[m] = 0u;
         }
         const uint32_t pitch_b = static_cast<uint32_t>(row_bytes);
-        int32_t i0 = seg_lo + wslot * kBlk + lane * V;
-        for (; i0 + V <= seg_hi; i0 += kStride) {
-          const uint4 tw = *reinterpret_cast<const uint4*>(tau_s + i0);
-          const uint4 cw = *reinterpret_cast<const uint4*>(acur_s + i0);
-          uint4 xw[M];
+        const char* rA = reinterpret_cast<const char*>(rowsA);
+        int32_t tail_i0 = -1;  // this lane's partial vector (n % 8 != 0), done after the loop
+        for (int32_t blk = grab(); blk < nblk;) {
+          const int32_t nxt = grab();  // claim ahead: the atomic overlaps this block
+          const int32_t i0 = seg_lo + blk * kBlk + lane * V;
+          if (i0 + V <= seg_hi) {
+            const uint4 tw = *reinterpret_cast<const uint4*>(tau_s + i0);
+            const uint4 cw = *reinterpret_cast<const uint4*>(acur_s + i0);
+            uint4 xw[M];
 #pragma unroll
-          for (int m = 0; m < M; ++m) xw[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
-          res_step_p32<M>(tw, cw, xw, i0, reinterpret_cast<const char*>(rowsA), pitch_b, ka, kj);
+            for (int m = 0; m < M; ++m) xw[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
+            res_step_p32<M>(tw, cw, xw, i0, rA, pitch_b, ka, kj);
+          } else if (i0 < seg_hi) {
+            tail_i0 = i0;
+          }
+          blk = nxt;
         }
         // keys -> tracks with s restored (packed32 keys carry d' = d + s)
 #pragma unroll
@@ -341,25 +382,31 @@ __global__ void __launch_bounds__(kResThreads, 1)
           ta[m].k = ka[m] ? ka[m] - sh : 0u;
           tj[m].k = kj[m] ? kj[m] - sh : 0u;
         }
-        if (i0 < seg_hi) {  // ragged tail (n % 8 != 0): generic body
+        if (tail_i0 >= 0) {  // ragged tail: generic body
           StreamRegs<E, M> r;
-          lds_tau<E>(tau_s + i0, r.t);
-          r.c = *reinterpret_cast<const uint4*>(acur_s + i0);
+          lds_tau<E>(tau_s + tail_i0, r.t);
+          r.c = *reinterpret_cast<const uint4*>(acur_s + tail_i0);
 #pragma unroll
-          for (int m = 0; m < M; ++m) r.x[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
-          compute_step<E, M, KM, false>(r, i0, seg_hi - i0, rowsA, ld, 0, sv, ta, tj);
+          for (int m = 0; m < M; ++m)
+            r.x[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + tail_i0);
+          compute_step<E, M, KM, false>(r, tail_i0, seg_hi - tail_i0, rowsA, ld, 0, sv, ta, tj);
         }
       } else {
-        for (int32_t i0 = seg_lo + wslot * kBlk + lane * V; i0 < seg_hi; i0 += kStride) {
-          StreamRegs<E, M> r;
-          lds_tau<E>(tau_s + i0, r.t);
-          r.c = *reinterpret_cast<const uint4*>(acur_s + i0);
+        for (int32_t blk = grab(); blk < nblk;) {
+          const int32_t nxt = grab();
+          const int32_t i0 = seg_lo + blk * kBlk + lane * V;
+          if (i0 < seg_hi) {
+            StreamRegs<E, M> r;
+            lds_tau<E>(tau_s + i0, r.t);
+            r.c = *reinterpret_cast<const uint4*>(acur_s + i0);
 #pragma unroll
-          for (int m = 0; m < M; ++m) r.x[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
-          if (i0 + V <= seg_hi)  // whole vector: branch-free body, gathers overlap
-            compute_step<E, M, KM, false>(r, i0, V, rowsA, ld, 0, sv, ta, tj);
-          else
-            compute_step<E, M, KM, false>(r, i0, seg_hi - i0, rowsA, ld, 0, sv, ta, tj);
+            for (int m = 0; m < M; ++m) r.x[m] = *reinterpret_cast<const uint4*>(rowsT + static_cast<size_t>(m) * ld + i0);
+            if (i0 + V <= seg_hi)  // whole vector: branch-free body, gathers overlap
+              compute_step<E, M, KM, false>(r, i0, V, rowsA, ld, 0, sv, ta, tj);
+            else
+              compute_step<E, M, KM, false>(r, i0, seg_hi - i0, rowsA, ld, 0, sv, ta, tj);
+          }
+          blk = nxt;
         }
       }
 
@@ -419,6 +466,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[b]);
+        if (st.tl_cap > 8192 && blockIdx.x == 0 && lane == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 12);
 
         bool finalize = (S == 1);
         if (S > 1) {

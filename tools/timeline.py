@@ -15,7 +15,7 @@ ap.add_argument("--solves", type=int, default=3)
 a = ap.parse_args()
 ctx = g.Context(0)
 ctx.generate(a.kind, a.n, 0)
-ctx.set_timeline(1 << 14)
+ctx.set_timeline(8192)
 names = {1: "full_sweep", 2: "scan", 3: "commit:start", 4: "commit:end", 5: "single:loaded",
          6: "single:round_end", 7: "res:tau16", 8: "res:acur", 9: "res:stage0", 10: "res:cta0_done",
          11: "cl:P1done", 12: "cl:round_end", 13: "cl:P3done", 14: "cl:P4done", 15: "apply"}
@@ -35,7 +35,7 @@ for k in range(a.solves):
 # raw sequence of the last solve's final iterations
 if tl:
     t0 = tl[0][0]
-    print("raw tail:", [(round((t - t0) / 1e3, 2), names.get(k, k)) for t, k in tl[-70:]])
+    print("raw tail:", [(round((t - t0) / 1e3, 2), names.get(k, k)) for t, k in tl[:80]])
 # resolution check
 ts = sorted(t for t, _ in tl)
 d = [b - a for a, b in zip(ts, ts[1:]) if b > a]
