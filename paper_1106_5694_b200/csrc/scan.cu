@@ -71,6 +71,16 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     if (p.m == 0) {  // one row per CTA does not fit twice: one 512-thread CTA per SM
       p.m = 1;
       p.threads = 512;
+      // LSAPGPU_SCAN_SPLIT=1: stage the gathered row in two half-row passes,
+      // double-buffered (measured 2x slower at C4: every pass scans every
+      // position, so it is off by default).
+      int split = 0;
+      if (const char* sp = std::getenv("LSAPGPU_SCAN_SPLIT")) split = std::atoi(sp);
+      if (split && force_bufs == 0) {
+        p.passes = 2;
+        p.chunk = ((d.ld + 1) / 2 + 63) / 64 * 64;
+        p.bufs = 2;
+      }
     } else {
       p.threads = 256;
     }
@@ -78,10 +88,11 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     if (force_bufs >= 1 && force_bufs <= 4 && static_cast<size_t>(force_bufs) * p.m * row <= budget)
       p.bufs = force_bufs;
     if (const char* t = std::getenv("LSAPGPU_SCAN_NT")) p.threads = std::atoi(t) == 256 ? 256 : 512;
-  } else {
+  } else {  // row longer than the budget: single-buffered chunks (every pass rescans all positions)
     p.m = 1;
     p.bufs = 1;
-    p.passes = static_cast<int>((row + budget - 1) / budget);
+    const size_t per_buf = budget;
+    p.passes = static_cast<int>((row + per_buf - 1) / per_buf);
     int64_t ch = (d.ld + p.passes - 1) / p.passes;
     ch = (ch + 63) / 64 * 64;
     p.chunk = ch;
