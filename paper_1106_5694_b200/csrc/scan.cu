@@ -13,6 +13,19 @@ template <class E, int KM>
 cudaError_t launch_scan_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
 template <class E, int KM>
 cudaError_t launch_scan_res_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+template <class E, int KM>
+cudaError_t launch_scan_cl_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+
+// Cluster kernel geometry (scan_cluster.cuh): per CTA a resident tau (int32) and
+// acur slice of L elements and two stages of (A slice, AT slice).
+size_t cl_smem_bytes(int32_t L, size_t es, int CS) {
+  const size_t slice = (static_cast<size_t>(L) * es + 127) / 128 * 128;
+  const size_t tau = (static_cast<size_t>(L) * 4 + 127) / 128 * 128;
+  return tau + slice + 2 * 2 * slice + 10 * 8 + 2 * 15 * 2 * 16 + 2 * CS * 2 * 16;
+}
+
+// Clusters of CS 512-thread CTAs with `smem` bytes each that can be resident at once.
+int cl_active_clusters(int CS, size_t smem);
 
 // Resident-state kernel geometry (scan_resident.cuh): 15 consumer warps + 1
 // producer, tau16 + acur resident, double-buffered (A row, AT row) stages.
@@ -106,11 +119,46 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
   if (p.max_segments < 1) p.max_segments = 1;
   if (p.max_segments > 16) p.max_segments = 16;
   if (const char* s = std::getenv("LSAPGPU_SCAN_SEGMENTS")) p.max_segments = std::atoi(s);
+  // streaming kernel: two vector steps in flight for float storage (fp64
+  // tracks leave registers for one more stream set), one for integer keys
+  p.depth = (d.storage == kF32 || d.storage == kF64) && p.m <= 2 ? 3 : 2;
+  if (const char* dd = std::getenv("LSAPGPU_SCAN_DEPTH")) p.depth = std::atoi(dd) == 3 ? 3 : 2;
+  // Cluster kernel (scan_cluster.cuh, opt-in: LSAPGPU_SCAN_CLUSTER=N CTAs per
+  // item): splits each row over N CTAs so rows that cannot be double-buffered
+  // on one SM stream while they are scanned.  Measured on B200 at C4 it is 4x
+  // SLOWER than the streaming kernel (full sweep 11.1 vs 2.77 ms): the random
+  // gathers through distributed shared memory (75 % remote at N = 4) run at
+  // ~1 us each under load.  Kept as a measured alternative, off by default.
+  {
+    int want = 0;
+    if (const char* c = std::getenv("LSAPGPU_SCAN_CLUSTER")) want = std::atoi(c);
+    const bool single_buffered = p.passes > 1 || (p.m == 1 && p.threads == 512 && p.bufs == 1);
+    if (want != 0 && !std::getenv("LSAPGPU_SCAN_BUDGET") && (single_buffered || want > 0)) {
+      const size_t limit = 210 * 1024;
+      for (int cs : {2, 4}) {
+        if (want > 0 && cs != want) continue;
+        int32_t L = static_cast<int32_t>((d.ld + cs - 1) / cs);
+        L = (L + 63) / 64 * 64;
+        const size_t sm = cl_smem_bytes(L, es, cs);
+        if (sm > limit) continue;
+        const int clusters = cl_active_clusters(cs, sm);
+        if (clusters <= 0) continue;
+        p.cluster = cs;
+        p.chunk = L;
+        p.smem = sm;
+        p.ctas = clusters * cs;
+        p.m = 1;
+        p.passes = 1;
+        p.threads = 512;
+        break;
+      }
+    }
+  }
   // Resident-state kernel when tau16 + acur + two (A, AT) stages fit on chip
   // (LSAPGPU_SCAN_RESIDENT=0 forces the streaming kernel).
   int resident = 1;
   if (const char* r = std::getenv("LSAPGPU_SCAN_RESIDENT")) resident = std::atoi(r);
-  if (resident && d.n < 65536 && d.tau16 && !std::getenv("LSAPGPU_SCAN_BUDGET")) {
+  if (resident && p.cluster == 0 && d.n < 65536 && d.tau16 && !std::getenv("LSAPGPU_SCAN_BUDGET")) {
     const size_t limit = 227 * 1024 - 14 * 1024;
     int m = 0;
     for (int mm : {4, 2, 1})
@@ -146,6 +194,17 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
 }
 
 cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  if (p.cluster > 0) {
+    switch (d.storage) {
+      case kI16:
+        return d.n <= 16384 ? launch_scan_cl_typed<int16_t, kPacked32>(d, p, full, st)
+                            : launch_scan_cl_typed<int16_t, kPacked64>(d, p, full, st);
+      case kI32: return launch_scan_cl_typed<int32_t, kPacked64>(d, p, full, st);
+      case kF32: return launch_scan_cl_typed<float, kFloat>(d, p, full, st);
+      case kF64: return launch_scan_cl_typed<double, kFloat>(d, p, full, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.resident) {
     switch (d.storage) {
       case kI16:

@@ -275,7 +275,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 constexpr int kEdgeBuf = 256;
 constexpr int kMaxBufs = 4;
 
-template <class E, int M, int NT, int KM, bool kChunked>
+template <class E, int M, int NT, int KM, bool kChunked, int D>
 __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, int full, int passes,
                                                           int64_t chunk, int bufs, int max_segments) {
   using Acc = typename Traits<E>::Acc;
@@ -430,20 +430,27 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
     const int32_t full_hi = seg_lo + ((seg_hi - seg_lo) / V) * V;
     const E* rows = stage_base + static_cast<size_t>(b) * M * chunk;
 
-    // main loop over whole vectors, stream registers one step ahead
-    // (unrolled twice over two register sets so no stream registers are copied)
+    // main loop over whole vectors: a ring of D stream-register sets keeps
+    // the next D-1 vector steps' loads in flight (fully unrolled, so every
+    // set stays in registers)
     int32_t i0 = seg_lo + tid * V;
-    StreamRegs<E, M> ra, rb;
-    if (i0 < full_hi) load_step<E, M>(ra, tau, acur, xrow, i0);
-    while (i0 < full_hi) {
-      const int32_t i1 = i0 + NT * V;
-      if (i1 < full_hi) load_step<E, M>(rb, tau, acur, xrow, i1);
-      compute_step<E, M, KM, kChunked>(ra, i0, V, rows, chunk, clo, sv, ta, tj);
-      if (i1 >= full_hi) break;
-      const int32_t i2 = i1 + NT * V;
-      if (i2 < full_hi) load_step<E, M>(ra, tau, acur, xrow, i2);
-      compute_step<E, M, KM, kChunked>(rb, i1, V, rows, chunk, clo, sv, ta, tj);
-      i0 = i2;
+    StreamRegs<E, M> rr[D];
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d)
+      if (i0 + d * NT * V < full_hi) load_step<E, M>(rr[d], tau, acur, xrow, i0 + d * NT * V);
+    for (bool more = i0 < full_hi; more;) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int32_t ic = i0 + d * NT * V;
+        if (ic >= full_hi) {
+          more = false;
+          break;
+        }
+        const int32_t ipf = ic + (D - 1) * NT * V;
+        if (ipf < full_hi) load_step<E, M>(rr[(d + D - 1) % D], tau, acur, xrow, ipf);
+        compute_step<E, M, KM, kChunked>(rr[d], ic, V, rows, chunk, clo, sv, ta, tj);
+      }
+      i0 += D * NT * V;
     }
     // ragged tail (only the last segment when n % V != 0)
     if (full_hi < seg_hi && tid == 0) {
@@ -593,7 +600,8 @@ constexpr size_t kStaticSmem = 14 * 1024;  // ebuf + item metadata + counters (+
 
 template <class E, int M, int NT, int KM>
 cudaError_t launch_nt(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  auto k = p.passes > 1 ? pair_scan_kernel<E, M, NT, KM, true> : pair_scan_kernel<E, M, NT, KM, false>;
+  auto k = p.passes > 1 ? pair_scan_kernel<E, M, NT, KM, true, 2>
+                        : (p.depth == 3 ? pair_scan_kernel<E, M, NT, KM, false, 3> : pair_scan_kernel<E, M, NT, KM, false, 2>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;

@@ -116,6 +116,8 @@ def test_generators_match_oracle(oracle, gpu_ctx):
     {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
     {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
+    {"LSAPGPU_SCAN_CLUSTER": "2"},                                     # row split over a 2-CTA cluster (opt-in)
+    {"LSAPGPU_SCAN_CLUSTER": "4"},                                     # ... 4 CTAs
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "1"},             # streaming kernel
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "2"},
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "4"},
