@@ -145,6 +145,91 @@ __global__ void build_layout_kernel(Src src, int64_t row0, int64_t rows, E* A, E
   }
 }
 
+// Fused layout pass: classify (flags as classify_kernel) and build (narrow +
+// transpose as build_layout_kernel) in ONE read of the source, for a storage
+// type speculated from the first rows (the caller rebuilds in the rare case
+// the flags demand a wider type).  64x64 tiles, 256 threads: each lane owns
+// two adjacent columns, so the source reads, the A-row writes and the AT-row
+// writes are all coalesced.
+template <class E>
+__global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0, int64_t rows, E* A, E* AT,
+                                                           int64_t ld, uint32_t* flags) {
+  __shared__ E tile[64][66];
+  const int64_t bi = row0 + static_cast<int64_t>(blockIdx.y) * 64;  // agent block
+  const int64_t bj = static_cast<int64_t>(blockIdx.x) * 64;         // job block
+  const int n = src.n;
+  const int64_t rend = row0 + rows;
+  const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;  // 8 row groups
+  const int64_t j = bj + 2 * lane;
+  uint32_t f = 0;
+  for (int r = rg; r < 64; r += 8) {
+    const int64_t i = bi + r;
+    if (i >= rend) break;
+    double v0 = 0.0, v1 = 0.0;
+    if (src.s.kind == 0 && src.s.src_dtype == 0 && j + 1 < n) {
+      // fp64 memory source: both columns in one 16-byte load when aligned
+      const double* p = static_cast<const double*>(src.s.src) + i * n + j;
+      if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const double2 w = __ldg(reinterpret_cast<const double2*>(p));
+        v0 = w.x;
+        v1 = w.y;
+      } else {
+        v0 = p[0];
+        v1 = p[1];
+      }
+    } else {
+      if (j < n) v0 = src(i, j);
+      if (j + 1 < n) v1 = src(i, j + 1);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double v = h ? v1 : v0;
+      if (j + h >= n) continue;
+      if (!isfinite(v)) {
+        f |= 1u | 2u | 4u | 8u;
+      } else {
+        const bool integral = v == trunc(v);
+        if (!(integral && fabs(v) <= 32767.0)) f |= 2u;
+        if (!(integral && fabs(v) < 536870912.0)) f |= 4u;
+        if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
+      }
+    }
+    const E e0 = narrow<E>(isfinite(v0) ? v0 : 0.0), e1 = narrow<E>(isfinite(v1) ? v1 : 0.0);
+    if (j + 1 < n) {
+      E* a = A + i * ld + j;
+      a[0] = e0;
+      a[1] = e1;
+    } else if (j < n) {
+      A[i * ld + j] = e0;
+    }
+    tile[r][2 * lane] = e0;
+    tile[r][2 * lane + 1] = e1;
+  }
+  __syncthreads();
+  // AT rows bj .. bj+63, columns (agents) bi .. bi+63
+  const int64_t ia = bi + 2 * lane;
+  for (int c = rg; c < 64; c += 8) {
+    const int64_t jj = bj + c;
+    if (jj >= n) break;
+    E* at = AT + jj * ld + ia;
+    if (ia + 1 < rend) {
+      at[0] = tile[2 * lane][c];
+      at[1] = tile[2 * lane + 1][c];
+    } else if (ia < rend) {
+      at[0] = tile[2 * lane][c];
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
+  __shared__ uint32_t wf[8];
+  if (lane == 0) wf[rg] = f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (int w = 0; w < 8; ++w) r |= wf[w];
+    if (r) atomicOr(flags, r);
+  }
+}
+
 template <class E>
 __global__ void init_assignment_kernel(DevState d) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -194,6 +279,13 @@ struct BuildK {
   }
 };
 template <class E>
+struct FusedK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, Src s, int64_t r0, int64_t rows, void* A, void* AT,
+                  int64_t ld, uint32_t* flags) {
+    layout_fused_kernel<E><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags);
+  }
+};
+template <class E>
 struct InitK {
   static void run(dim3 g, dim3 b, cudaStream_t st, DevState d) {
     init_assignment_kernel<E><<<g, b, 0, st>>>(d);
@@ -236,6 +328,13 @@ cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, 
   Src src{s, n};
   dim3 g(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
   return dispatch<BuildK>(storage, g, dim3(32, 8), st, src, row0, rows, A, AT, ld);
+}
+
+cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
+                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st) {
+  Src src{s, n};
+  dim3 g(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
+  return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags);
 }
 
 cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st) {

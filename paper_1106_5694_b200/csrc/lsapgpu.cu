@@ -335,25 +335,39 @@ void finish_matrix(lsapgpu_ctx* ctx, int32_t n) {
 }
 
 // Builds A/AT from a layout source; src_rows_dev is a device pointer for memory sources.
+// The storage type is speculated from the first 64 rows, then ONE fused pass
+// classifies every entry and builds A / AT; only if a later row needs a wider
+// type is the layout rebuilt.
 int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   int rc = ensure_vectors(ctx, n);
   if (rc) return rc;
   ctx->n_matrix = 0;
   drop_graph(ctx);
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(uint32_t), ctx->stream));
-  CK(launch_classify(src, n, 0, n, ctx->flags_dev, ctx->stream));
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, 2 * sizeof(uint32_t), ctx->stream));
+  const int64_t probe = std::min<int64_t>(64, n);
+  CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream));
   ++ctx->launches;
   uint32_t flags = 0;
   CK(cpy(ctx, &flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
-  const int storage = storage_of_flags(flags);
-  if ((rc = alloc_matrix(ctx, n, storage))) return rc;
+  const int spec = storage_of_flags(flags);
+  if ((rc = alloc_matrix(ctx, n, spec))) return rc;
   DevState& d = ctx->d;
-  CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
-                         ctx->stream));
+  CK(launch_layout_fused(src, n, 0, n, spec, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
+                         ctx->flags_dev + 1, ctx->stream));
   ++ctx->launches;
+  CK(cpy(ctx, &flags, ctx->flags_dev + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+  const int storage = storage_of_flags(flags);
+  if (storage != spec) {
+    if ((rc = alloc_matrix(ctx, n, storage))) return rc;
+    CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
+                           ctx->stream));
+    ++ctx->launches;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   finish_matrix(ctx, n);
   return LSAPGPU_OK;
 }
@@ -441,9 +455,9 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
     }
     CK(cudaEventRecord(done, ctx->copy_stream));
     CK(cudaStreamWaitEvent(ctx->stream, done, 0));
-    CK(launch_classify(src, n, r0, rows, ctx->chunk_flags + k, ctx->stream));
-    ++ctx->launches;
-    if (k == 0) {  // speculate the storage from the first chunk
+    if (k == 0) {  // speculate the storage from the first rows
+      CK(launch_classify(src, n, r0, std::min<int64_t>(rows, 64), ctx->chunk_flags + k, ctx->stream));
+      ++ctx->launches;
       uint32_t f0 = 0;
       CK(cpy(ctx, &f0, ctx->chunk_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
@@ -457,8 +471,8 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
         return rc;
       }
     }
-    CK(launch_build_layout(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
-                           const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->stream));
+    CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
+                           const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->chunk_flags + k, ctx->stream));
     ++ctx->launches;
   }
   std::vector<uint32_t> fl(nchunks);
@@ -625,7 +639,7 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||
-      cudaMalloc(&ctx->flags_dev, sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&ctx->flags_dev, 2 * sizeof(uint32_t)) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming) != cudaSuccess) {
