@@ -183,6 +183,7 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       p.ctas = num_sms;
       // splitting items over CTAs re-stages whole rows per segment and adds a
       // cross-CTA merge; measured slower than whole items at every list size
+      // (even lists shorter than the grid), so it is opt-in
       p.max_segments = 1;
       if (const char* sg = std::getenv("LSAPGPU_SCAN_SEGMENTS")) p.max_segments = std::atoi(sg);
       p.l2_prefetch = 0;  // measured slower at every distance (tools/ab.py)

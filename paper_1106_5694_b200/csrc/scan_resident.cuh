@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const uint32_t* __restrict__ items = st.use_own ? st.items_own : st.items;
   const int32_t groups = (count + M - 1) / M;
   int S = 1;  // segments per item group (short lists): best whole-wave fill
-  {
+  if (groups < static_cast<int32_t>(gridDim.x)) {  // only lists that leave SMs idle
     const int G = gridDim.x;
     float best_eff = -1.f;
     for (int s = 1; s <= max_segments; ++s) {
