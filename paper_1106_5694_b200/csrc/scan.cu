@@ -15,6 +15,16 @@ template <class E, int KM>
 cudaError_t launch_scan_res_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
 template <class E, int KM>
 cudaError_t launch_scan_cl_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+template <class E, int KM>
+cudaError_t launch_scan_big_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+
+// Staged-row + chunk-ring kernel geometry (scan_big.cuh): the whole A row plus
+// two position chunks of (AT, acur, tau16).
+size_t big_smem_bytes(int64_t ld, size_t es, int32_t C) {
+  const size_t row = (static_cast<size_t>(ld) * es + 127) / 128 * 128;
+  const size_t slot = (static_cast<size_t>(C) * (2 * es + 2) + 127) / 128 * 128;
+  return row + 2 * slot + 6 * 8 + 14 * 2 * 16;
+}
 
 // Cluster kernel geometry (scan_cluster.cuh): per CTA a resident tau (int32) and
 // acur slice of L elements and two stages of (A slice, AT slice).
@@ -191,10 +201,43 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       if (p.l2_prefetch >= 32 / m) p.l2_prefetch = 32 / m - 1;
     }
   }
+  // Rows that fit on chip once but not twice (C4): stage the row whole and
+  // stream AT / acur / tau16 through a TMA chunk ring (scan_big.cuh).  Opt-in
+  // (LSAPGPU_SCAN_BIG=1): measured at C4 it is ~10 % slower than the
+  // streaming kernel, whose bound there is the fp64 compare-select work of
+  // float storage, not the stream.
+  int big = 0;
+  if (const char* bg = std::getenv("LSAPGPU_SCAN_BIG")) big = std::atoi(bg);
+  if (big && !p.resident && !p.cluster && d.tau16 && d.n < 65536 && !std::getenv("LSAPGPU_SCAN_BUDGET") &&
+      (p.passes > 1 || (p.m == 1 && p.threads == 512) || big > 1)) {
+    for (int32_t C : {4096, 2048, 1024}) {
+      const size_t sm = big_smem_bytes(d.ld, es, C);
+      if (sm > 210 * 1024) continue;
+      p.big = 1;
+      p.chunk = C;
+      p.smem = sm;
+      p.ctas = num_sms;
+      p.m = 1;
+      p.passes = 1;
+      p.threads = 512;
+      break;
+    }
+  }
   return p;
 }
 
 cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  if (p.big) {
+    switch (d.storage) {
+      case kI16:
+        return d.n <= 16384 ? launch_scan_big_typed<int16_t, kPacked32>(d, p, full, st)
+                            : launch_scan_big_typed<int16_t, kPacked64>(d, p, full, st);
+      case kI32: return launch_scan_big_typed<int32_t, kPacked64>(d, p, full, st);
+      case kF32: return launch_scan_big_typed<float, kFloat>(d, p, full, st);
+      case kF64: return launch_scan_big_typed<double, kFloat>(d, p, full, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.cluster > 0) {
     switch (d.storage) {
       case kI16:

@@ -155,7 +155,8 @@ struct Track<kFloat> {
     i = INT_MAX;
   }
   __device__ __forceinline__ void add(double v, int32_t idx) {
-    const bool take = (v > d) || (v == d && idx < i);
+    // branch-free: predicates combined with bitwise ops (no short-circuit jumps)
+    const bool take = (v > d) | ((v == d) & (idx < i));
     d = take ? v : d;
     i = take ? idx : i;
   }
@@ -218,6 +219,7 @@ __device__ __forceinline__ void compute_step(const StreamRegs<E, M>& r, int32_t 
                                              const E* __restrict__ rows, int64_t chunk, int64_t clo,
                                              const typename Traits<E>::Acc (&sv)[M], Track<KM> (&ta)[M],
                                              Track<KM> (&tj)[M]) {
+
   using Acc = typename Traits<E>::Acc;
   constexpr int V = StreamRegs<E, M>::V;
 #pragma unroll

@@ -116,6 +116,7 @@ struct ScanPlan {
   size_t smem = 0;      // dynamic smem per CTA
   int max_segments = 1;
   int resident = 0;     // 1: resident-state kernel (scan_resident.cuh)
+  int big = 0;          // 1: staged-row + chunk-ring kernel (scan_big.cuh); chunk = positions per chunk
   int cluster = 0;      // > 0: cluster kernel (scan_cluster.cuh) with this many CTAs per item; chunk = slice
   int depth = 2;        // streaming kernel: vector steps of the streamed rows in flight
   int l2_prefetch = 0;  // resident kernel: stages whose rows are prefetched into L2 ahead

@@ -118,9 +118,10 @@ def test_generators_match_oracle(oracle, gpu_ctx):
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
     {"LSAPGPU_SCAN_CLUSTER": "2"},                                     # row split over a 2-CTA cluster (opt-in)
     {"LSAPGPU_SCAN_CLUSTER": "4"},                                     # ... 4 CTAs
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_BIG": "2"},          # staged row + TMA chunk ring (opt-in)
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "1"},             # streaming kernel
-    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "2"},
-    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "4"},
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_BIG": "0", "LSAPGPU_SCAN_M": "2"},
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_BIG": "0", "LSAPGPU_SCAN_M": "4"},
     {"LSAPGPU_SCAN_BUDGET": "3072"},                                   # streaming, chunked passes
     {"LSAPGPU_SCAN_BUDGET": "9000", "LSAPGPU_SCAN_M": "1"},            # streaming, single-buffered rows
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_SEGMENTS": "8"},      # streaming, split items
