@@ -277,7 +277,20 @@ def run_ours(args, wl) -> None:
             e2e_ms = float(t.item())
         e2e = {"value": e2e_ms, "unit": "ms",
                "h2d_bytes_per_step": (e1["h2d_bytes"] - e0["h2d_bytes"]) // args.steps,
-               "d2h_bytes_per_step": (e1["d2h_bytes"] - e0["d2h_bytes"]) // args.steps}
+               "d2h_bytes_per_step": (e1["d2h_bytes"] - e0["d2h_bytes"]) // args.steps,
+               "source": "pinned host fp64 (the caller's buffer, DMA'd directly)"}
+        # the same call from pageable memory (a plain std::vector / numpy
+        # Instance, what a drop-in caller of the C++ API passes): staged
+        # through the pinned ring by the host copy threads
+        a_pageable = a_host.numpy().copy()
+
+        def step_pageable():
+            ctx.set_matrix(a_pageable)
+            return ctx.solve(cfg, trace=False)
+
+        step_pageable()
+        ptimes, _ = timed(step_pageable, max(1, min(args.steps, 5)))
+        e2e["pageable_ms"] = statistics.mean(ptimes)
 
     # roofline of the dominant kernel (pair scan): instrumented host-stepped solve,
     # every scan launch bracketed by CUDA events on the solver's stream
