@@ -196,19 +196,36 @@ def run_ours(args, wl) -> None:
     import torch
 
     rank, world, local = dist_env()
+    if args.backend == "gloo":
+        local = 0  # every rank on GPU 0 (tests of the multi-rank path on one device)
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # gloo: several ranks sharing one GPU (tests of the sharded path)
+            dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     import paper_1106_5694_b200 as g
 
     kind, n, iseed, param, desc = wl
-    # replicas: every rank solves its own instance (seed offset by rank); see DESIGN.md "Multi-GPU"
-    iseed = iseed + rank
+    # N > 1: by default ONE instance is solved by all ranks (the sharded solve
+    # of DESIGN.md §7: scan items owned by agent index, per-batch record
+    # allgather, replicated commit); --replicas: every rank solves its own
+    # instance (seed offset by rank)
+    sharded = world > 1 and not args.replicas
+    if world > 1 and not sharded:
+        iseed = iseed + rank
     ctx = g.Context(local)
     cfg = g.ParallelConfig(seed=0)
     stream = torch.cuda.ExternalStream(ctx.stream)
+    exch = None
+    if sharded:
+        from paper_1106_5694_b200.dist import TorchDistExchange
+        exch = TorchDistExchange()
+
+    def solve():
+        return ctx.solve(cfg, trace=False, dist=exch)
 
     # the input instance (fp64 host matrix, like lsap::Instance), built by the
     # package's on-device generator (same recipe and bits as the reference's)
@@ -222,11 +239,11 @@ def run_ours(args, wl) -> None:
 
     def step_device():
         ctx.set_matrix(a_dev)
-        return ctx.solve(cfg, trace=False)
+        return solve()
 
     def step_e2e():
         ctx.set_matrix(a_host.numpy())
-        return ctx.solve(cfg, trace=False)
+        return solve()
 
     def barrier():
         if world > 1:
@@ -246,7 +263,7 @@ def run_ours(args, wl) -> None:
             times.append(ev0.elapsed_time(ev1))
         return times, rep
 
-    step = step_device if a_dev is not None else (lambda: ctx.solve(cfg, trace=False))
+    step = step_device if a_dev is not None else solve
     for _ in range(args.warmup):
         step()
     c0 = ctx.counters()
@@ -257,7 +274,7 @@ def run_ours(args, wl) -> None:
     c1 = ctx.counters()
     ms = statistics.mean(times)
     if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
+        t = torch.tensor([ms], device=f"cuda:{local}" if args.backend == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     launches = (c1["kernel_launches"] - c0["kernel_launches"]) // max(args.steps, 1)
@@ -272,7 +289,7 @@ def run_ours(args, wl) -> None:
         e1 = ctx.counters()
         e2e_ms = statistics.mean(etimes)
         if world > 1:
-            t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+            t = torch.tensor([e2e_ms], device=f"cuda:{local}" if args.backend == "nccl" else "cpu")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": e2e_ms, "unit": "ms",
@@ -286,7 +303,7 @@ def run_ours(args, wl) -> None:
 
         def step_pageable():
             ctx.set_matrix(a_pageable)
-            return ctx.solve(cfg, trace=False)
+            return solve()
 
         step_pageable()
         ptimes, _ = timed(step_pageable, max(1, min(args.steps, 5)))
@@ -330,12 +347,16 @@ def run_ours(args, wl) -> None:
     clocks = clk.summary()
     out = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": {"int16": "i16->i32", "int32": "i32", "fp32": "f32->f64",
                                        "fp64": "f64"}[ctx.storage],
         "data": "synthetic",
         "config": {"workload": desc, "n": n, "solver_seed": 0, "reeval": "touched_and_conflicted",
-                   "storage": ctx.storage, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "storage": ctx.storage,
+                   "parallelism": (f"sharded x{world}: scan items by agent index, {args.backend} record allgather, "
+                                   f"replicated commit" if sharded else
+                                   f"replicas x{world}" if world > 1 else "single"),
                    "l2": "inputs larger than L2 (8*n^2 B fp64 source + A/AT), no flush needed",
                    "step": "device-resident fp64 input -> layout -> dgs_parallel -> sigma/tau on host"},
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
@@ -361,6 +382,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent instances instead of one sharded solve")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1 process-group backend (gloo: ranks sharing one GPU, for tests)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

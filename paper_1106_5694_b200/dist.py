@@ -76,8 +76,17 @@ class TorchDistExchange(_Exchange):
         import torch
         import torch.distributed as dist
         s = torch.cuda.ExternalStream(stream, device=self.send.device)
+        if dist.get_backend(self.group) == "nccl":
+            with torch.cuda.stream(s):
+                dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            return
+        # host-staged exchange for CPU backends (gloo: several ranks per GPU in tests)
+        s.synchronize()
+        send = self.send.cpu()
+        recv = torch.empty(send.numel() * self.world, dtype=send.dtype)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
         with torch.cuda.stream(s):
-            dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            self.recv.copy_(recv, non_blocking=False)
 
 
 class ThreadExchange(_Exchange):

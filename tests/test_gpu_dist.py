@@ -55,3 +55,42 @@ def test_multi_rank_equals_single_gpu(oracle, gpu_ctx, kind, n, world, policy):
         assert rep.objective_trace == ref.objective_trace
         assert rep.outer_iterations == ref.outer_iterations
         assert rep.gpu["inner_iterations"] == ref.gpu["inner_iterations"]
+
+
+def test_torch_distributed_two_ranks(oracle, gpu_ctx, tmp_path):
+    """The torch.distributed exchange (TorchDistExchange) across two real
+    processes: gloo ranks sharing GPU 0, so the multi-process path bench.py
+    uses at N > 1 (NCCL on a multi-GPU node) runs here end to end and must
+    match the single-GPU solve bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    import paper_1106_5694_b200 as g
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    a = oracle.generate("int", 1500, 9)
+    np.save(tmp_path / "a.npy", a)
+    script = tmp_path / "rank.py"
+    script.write_text(
+        "import os, sys, numpy as np, torch, torch.distributed as dist\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_1106_5694_b200 as g\n"
+        "from paper_1106_5694_b200.dist import TorchDistExchange\n"
+        "dist.init_process_group('gloo')\n"
+        "torch.cuda.set_device(0)\n"
+        f"a = np.load({str(tmp_path / 'a.npy')!r})\n"
+        "ctx = g.Context(0); ctx.set_matrix(a)\n"
+        "ex = TorchDistExchange()\n"
+        "rep = ctx.solve(g.ParallelConfig(seed=4), dist=ex)\n"
+        f"np.save(os.path.join({str(tmp_path)!r}, 'sigma%d.npy' % dist.get_rank()), rep.assignment.sigma)\n"
+        "print('calls', ex.calls, 'value', rep.assignment.value)\n"
+        "dist.destroy_process_group()\n")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", str(script)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    gpu_ctx.set_matrix(a)
+    ref = gpu_ctx.solve(g.ParallelConfig(seed=4))
+    for rank in range(2):
+        sig = np.load(tmp_path / f"sigma{rank}.npy")
+        assert np.array_equal(sig, ref.assignment.sigma)
