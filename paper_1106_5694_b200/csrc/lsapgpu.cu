@@ -171,6 +171,12 @@ struct lsapgpu_ctx {
   // cumulative transfer / launch counters (bench.py's e2e and gpu_launches)
   int64_t h2d = 0, d2h = 0, launches = 0;
 
+  // pinned host mirrors for the solve's device->host reads (one sync each)
+  double* obj_pin = nullptr;     // per-job entries of the ordered objective
+  int32_t obj_cap = 0;
+  LogEntry* log_pin = nullptr;   // delta-log prefix drained with the control block
+  static constexpr int64_t kLogPin = 1 << 16;
+
   // host upload pipeline (lsapgpu_set_matrix)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_ready = nullptr;
@@ -508,6 +514,29 @@ bool is_perm(const int32_t* p, int32_t n) {
 }
 
 // Ordered objective (core.cpp:17-24) over the device matrix and a device sigma.
+// Enqueue the objective gather into pinned memory (no sync); objective_sum
+// adds it up in job order once the stream has been synchronised.
+int enqueue_objective(lsapgpu_ctx* ctx) {
+  const int32_t n = ctx->d.n;
+  if (ctx->obj_cap < n) {
+    if (ctx->obj_pin) cudaFreeHost(ctx->obj_pin);
+    ctx->obj_pin = nullptr;
+    ctx->obj_cap = 0;
+    CK(cudaMallocHost(&ctx->obj_pin, sizeof(double) * n));
+    ctx->obj_cap = n;
+  }
+  double* dv = reinterpret_cast<double*>(ctx->d.c_delta);  // scratch (2n doubles)
+  CK(launch_gather_current(ctx->d, dv, ctx->stream));
+  ++ctx->launches;
+  CK(cpy(ctx, ctx->obj_pin, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  return LSAPGPU_OK;
+}
+double objective_sum(const lsapgpu_ctx* ctx) {  // core.cpp:17-24: ordered sum over jobs
+  double sum = 0.0;
+  for (int32_t j = 0; j < ctx->d.n; ++j) sum += ctx->obj_pin[j];
+  return sum;
+}
+
 int device_objective(lsapgpu_ctx* ctx, double* value) {
   const int32_t n = ctx->d.n;
   double* dv = reinterpret_cast<double*>(ctx->d.c_delta);  // scratch (2n doubles)
@@ -672,6 +701,8 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->d.tl) cudaFree(ctx->d.tl);
+  if (ctx->obj_pin) cudaFreeHost(ctx->obj_pin);
+  if (ctx->log_pin) cudaFreeHost(ctx->log_pin);
   if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   if (ctx->stage.p) cudaFree(ctx->stage.p);
   if (ctx->chunk_flags) cudaFree(ctx->chunk_flags);
@@ -803,6 +834,8 @@ int lsapgpu_set_timeline(lsapgpu_ctx* ctx, int32_t capacity) {
   if (!ctx) return LSAPGPU_ERR_INVALID;
   CK(cudaSetDevice(ctx->device));
   if (ctx->d.tl) cudaFree(ctx->d.tl);
+  if (ctx->obj_pin) cudaFreeHost(ctx->obj_pin);
+  if (ctx->log_pin) cudaFreeHost(ctx->log_pin);
   ctx->d.tl = nullptr;
   ctx->d.tl_cap = 0;
   if (capacity > 0) {
@@ -1079,9 +1112,13 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   CK(cpy(ctx, d.sigma, sigma0.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(launch_init_assignment(d, ctx->stream));
   ++ctx->launches;
-  double value = 0.0;
-  int rc = device_objective(ctx, &value);
+  // initial objective and the counter base, read back with ONE sync
+  int rc = enqueue_objective(ctx);
   if (rc) return rc;
+  CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double value = objective_sum(ctx);
+  const Ctrl base = *ctx->ctrl_host;  // counters are cumulative per context
 
   TraceSink trace{trace_switch, trace_value, trace_cap};
   trace.push(0, value);
@@ -1109,14 +1146,12 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   }
   ctx->scan_ms = ctx->full_ms = ctx->commit_ms = 0.0;
   ctx->scan_launches = ctx->full_launches = ctx->commit_launches = 0;
-
-  rc = pull_ctrl(ctx);
-  if (rc) return rc;
-  const Ctrl base = *ctx->ctrl_host;  // counters are cumulative per context
+  if (!ctx->log_pin) CK(cudaMallocHost(&ctx->log_pin, sizeof(LogEntry) * lsapgpu_ctx::kLogPin));
   std::vector<LogEntry> log, sorted;
   int64_t switches = 0;
   int64_t launches = 0;
   int64_t graph_launches = 0;
+  bool prefetched = false;  // ctrl + log prefix already read back with the graph's sync
 
   while (!expired) {
     ++S.outer_iterations;
@@ -1150,8 +1185,12 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       } else if (P.use_graph) {
         CK(cudaGraphLaunch(ctx->exec, ctx->stream));
         ++graph_launches;
-        rc = pull_ctrl(ctx);
-        if (rc) return rc;
+        // control block and the first kLogPin log entries with one sync
+        CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cpy(ctx, ctx->log_pin, d.log, sizeof(LogEntry) * std::min<int64_t>(lsapgpu_ctx::kLogPin, d.log_cap),
+               cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        prefetched = true;
       } else {
         for (;;) {
           if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -1182,10 +1221,14 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       }
       const int64_t cnt = C.log_count;
       log.resize(static_cast<size_t>(cnt));
-      if (cnt) {
-        CK(cpy(ctx, log.data(), d.log, sizeof(LogEntry) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+      const int64_t have = prefetched ? std::min<int64_t>(cnt, lsapgpu_ctx::kLogPin) : 0;
+      if (have) std::memcpy(log.data(), ctx->log_pin, sizeof(LogEntry) * have);
+      if (cnt > have) {
+        CK(cpy(ctx, log.data() + have, d.log + have, sizeof(LogEntry) * (cnt - have), cudaMemcpyDeviceToHost,
+               ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
       }
+      prefetched = false;
       // Replay in the reference's batch order (iteration, then ascending slot:
       // agents then jobs, parallel.cpp:306-310).  Integer deltas sum exactly in
       // any order, so without a trace the order only matters for float storage.
@@ -1213,8 +1256,14 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     if (value == f_start) break;
   }
 
-  rc = pull_ctrl(ctx);
+  // final counters, sigma / tau and the ordered objective with ONE sync
+  CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tau_out) CK(cpy(ctx, tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  rc = enqueue_objective(ctx);  // snapshot_assignment, solver_state.hpp:141-148
   if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double final_value = objective_sum(ctx);
   const Ctrl& C = *ctx->ctrl_host;
   S.inner_iterations = C.inner_iterations - base.inner_iterations;
   S.pair_items += C.pair_items - base.pair_items;
@@ -1231,11 +1280,6 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 
-  CK(cpy(ctx, sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (tau_out) CK(cpy(ctx, tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  double final_value = 0.0;
-  rc = device_objective(ctx, &final_value);  // snapshot_assignment, solver_state.hpp:141-148
-  if (rc) return rc;
   S.value = final_value;
   S.elapsed_ms = static_cast<double>(elapsed_ns()) / 1e6;
   if (stats) *stats = S;
