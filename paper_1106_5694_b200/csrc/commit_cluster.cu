@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(kNT, 1)
       }
       return;
     }
-    if (rank == 0 && tid == 0) C->work_count = 0;  // appends start after two cluster barriers
+    if (rank == 0 && tid == 0) {
+      C->work_count = 0;  // appends start after two cluster barriers
+      C->k2_nlog = C->k2_nconf = 0;
+    }
   }
   // Default policy and a batch whose vertex state fits one SM: the conflict
   // check runs on one CTA with CTA barriers and local shared-memory atomics,
@@ -153,6 +156,10 @@ __global__ void __launch_bounds__(kNT, 1)
   for (int32_t x = tid; x < kslice; x += kNT) {
     mykeys[x] = 0u;
     myflags[x] = 0u;
+  }
+  if (mode == kCommitSolve && st.policy == 0) {  // this CTA's slice of the rejected-job bitmap
+    const int32_t words = (n + 31) / 32, wper = (words + CS - 1) / CS;
+    for (int32_t x = rank * wper + tid; x < min(words, (rank + 1) * wper); x += kNT) st.jbits[x] = 0u;
   }
   const int32_t per = (m + CS - 1) / CS;
   const int32_t e0 = rank * per;
@@ -269,6 +276,66 @@ __global__ void __launch_bounds__(kNT, 1)
       }
     if (rank == 0 && tid == 0) C->lfmm_rounds += rounds;
     cluster.sync();  // peers may still read our counters
+    return;
+  }
+
+  if (st.policy == 0) {
+    // Default policy: every proposal is fresh (commit_single.cuh), so
+    // committed == accepted and touched == matched; classify here and let
+    // commit_apply_kernel do the scattered writes grid-wide.
+    const int lane = tid & 31;
+    for (int32_t base = tid - lane; base < cnt; base += kNT) {
+      const int32_t l = base + lane;
+      const uint8_t s = l < cnt ? Ea.st[l] : kEdgeUndecided;
+      const bool acc = s == kEdgeAccepted;
+      const unsigned am = __ballot_sync(0xffffffffu, acc);
+      if (am) {
+        int r0 = 0;
+        if (lane == 0) r0 = atomicAdd(&C->k2_nlog, __popc(am));
+        r0 = __shfl_sync(0xffffffffu, r0, 0);
+        if (acc) st.clist[r0 + __popc(am & ((1u << lane) - 1))] = e0 + l;
+      }
+      if (s == kEdgeRejected && Ea.slot[l] >= n) {
+        const int32_t j = Ea.slot[l] - n;
+        atomicOr(&st.jbits[j >> 5], 1u << (j & 31));
+      }
+    }
+    cluster.sync();  // bitmap and committed list complete
+    for (int32_t base = tid - lane; base < cnt; base += kNT) {
+      const int32_t l = base + lane;
+      bool q = false;
+      if (l < cnt && Ea.st[l] == kEdgeRejected) {
+        const int32_t p = Ea.u[l];  // the proposer (the record's owner)
+        q = kbase[p % CS][p / CS] != kMatched && !(atomicOr(fbase[p % CS] + p / CS, kQueued) & kQueued);
+      }
+      const unsigned qm = __ballot_sync(0xffffffffu, q);
+      if (qm) {
+        int r0 = 0;
+        if (lane == 0) r0 = atomicAdd(&C->k2_nconf, __popc(qm));
+        r0 = __shfl_sync(0xffffffffu, r0, 0);
+        if (q) st.qlist[r0 + __popc(qm & ((1u << lane) - 1))] = e0 + l;
+      }
+    }
+    cluster.sync();  // counts final; peers done with this CTA's shared memory
+    if (rank == 0 && tid == 0) {
+      const int nlog = C->k2_nlog, nconf = C->k2_nconf, nitems = 2 * nlog + nconf;
+      C->k2_parity = P;
+      C->k2_iter = iter;
+      C->k2_log_base = C->log_count;
+      C->log_count += nlog;
+      C->work_count = nitems;
+      C->switches += nlog;
+      C->pair_items += nitems;
+      C->agent_scans += nitems;
+      C->job_scans += 2 * nlog;  // + queued proposers with a rejected job record (apply kernel)
+      C->iter = iter;
+      C->parity = 1 - P;
+      C->edge_count[P] = 0;
+      C->lfmm_rounds += rounds;
+      C->inner_iterations += 1;
+      if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
+      tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
+    }
     return;
   }
 
