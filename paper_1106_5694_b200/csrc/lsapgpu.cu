@@ -159,8 +159,11 @@ struct lsapgpu_ctx {
   // cached inner-loop graph
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
-  double graph_eps = -1.0;
-  int graph_policy = -1;
+  // everything the captured kernels took by value: a new matrix in the same
+  // buffers with the same plans (every bench step) reuses the graph
+  DevState graph_state;
+  ScanPlan graph_scan;
+  CommitPlan graph_commit;
 
   // scan timing (host-stepped mode)
   bool timing = false;
@@ -348,7 +351,6 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   int rc = ensure_vectors(ctx, n);
   if (rc) return rc;
   ctx->n_matrix = 0;
-  drop_graph(ctx);
   CK(cudaMemsetAsync(ctx->flags_dev, 0, 2 * sizeof(uint32_t), ctx->stream));
   const int64_t probe = std::min<int64_t>(64, n);
   CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream));
@@ -391,7 +393,6 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
   int rc = ensure_vectors(ctx, n);
   if (rc) return rc;
   ctx->n_matrix = 0;
-  drop_graph(ctx);
   const size_t es = src_size(dtype);
   const size_t row_bytes = static_cast<size_t>(n) * es;
   const size_t total = row_bytes * static_cast<size_t>(n);
@@ -573,8 +574,9 @@ int build_graph(lsapgpu_ctx* ctx) {
   CK(e1);
   CK(e2);
   CK(cudaGraphInstantiate(&ctx->exec, ctx->graph, 0));
-  ctx->graph_eps = ctx->d.eps;
-  ctx->graph_policy = ctx->d.policy;
+  ctx->graph_state = ctx->d;
+  ctx->graph_scan = ctx->scan_plan;
+  ctx->graph_commit = ctx->commit_plan;
   return LSAPGPU_OK;
 }
 
@@ -1139,7 +1141,9 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         ctx->ctrl_dev, P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns()));
     ++ctx->launches;
     CK(cudaGetLastError());
-    if (P.use_graph && !multi && (!ctx->exec || ctx->graph_eps != d.eps || ctx->graph_policy != d.policy)) {
+    if (P.use_graph && !multi &&
+        (!ctx->exec || std::memcmp(&ctx->graph_state, &d, sizeof(DevState)) != 0 ||
+         !(ctx->graph_scan == ctx->scan_plan) || !(ctx->graph_commit == ctx->commit_plan))) {
       rc = build_graph(ctx);
       if (rc) return rc;
     }

@@ -120,6 +120,11 @@ struct ScanPlan {
   int cluster = 0;      // > 0: cluster kernel (scan_cluster.cuh) with this many CTAs per item; chunk = slice
   int depth = 2;        // streaming kernel: vector steps of the streamed rows in flight
   int l2_prefetch = 0;  // resident kernel: stages whose rows are prefetched into L2 ahead
+  bool operator==(const ScanPlan& o) const {
+    return m == o.m && passes == o.passes && chunk == o.chunk && bufs == o.bufs && ctas == o.ctas &&
+           threads == o.threads && smem == o.smem && max_segments == o.max_segments && resident == o.resident &&
+           big == o.big && cluster == o.cluster && depth == o.depth && l2_prefetch == o.l2_prefetch;
+  }
 };
 ScanPlan plan_scan(const DevState& d, int num_sms);
 // full sweep (identity work list, count n) when full != 0, else the device work list
@@ -142,6 +147,10 @@ struct CommitPlan {
   size_t cluster_smem = 0;  // cluster kernel: dynamic smem per CTA
   int edge_cap = 0;         // cluster kernel: proposals per CTA held in smem
   int cta_edge_cap = 0;     // single-CTA path taken when the proposals fit one CTA (0: never)
+  bool operator==(const CommitPlan& o) const {
+    return threads == o.threads && smem == o.smem && keys_in_smem == o.keys_in_smem && cluster == o.cluster &&
+           cluster_smem == o.cluster_smem && edge_cap == o.edge_cap && cta_edge_cap == o.cta_edge_cap;
+  }
 };
 CommitPlan plan_commit(const DevState& d);
 cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
