@@ -14,6 +14,8 @@
  *                                   (parallel.hpp:71-74, parallel.cpp:182-229)
  *   lsapgpu_set_matrix              replaces Instance::validate + SolverState::build_columns
  *                                   (src/core.cpp:9-15, src/solver_state.hpp:67-76)
+ *   lsapgpu_auction_solve           replaces lsap::auction_solve, the paper's comparator
+ *                                   (include/lsap/baselines.hpp:12-36, src/auction.cpp:110-153)
  *   lsapgpu_random_perm / lsapgpu_objective
  *                                   host helpers equal to lsap::random_perm (include/lsap/rng.hpp:37-46)
  *                                   and lsap::objective (src/core.cpp:17-24)
@@ -174,6 +176,42 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
                                     double eps, int32_t* applied_agent, int32_t* applied_new_job,
                                     int32_t* applied_old_job, int32_t* applied_displaced,
                                     double* applied_delta, int32_t* n_applied);
+
+/* lsap::auction_solve: synchronous bidding rounds on the
+ * context's matrix, every round of every epsilon phase inside one launch.
+ * AuctionConfig (baselines.hpp:12-26): epsilon is used when has_epsilon
+ * (else (max - min) / (2n), or 1.0 for a constant matrix); scaling /
+ * scale_factor select epsilon scaling; deadline_ns < 0 = none, on expiry the
+ * partial assignment is completed greedily (terminated_by 1,
+ * completed_greedily 1).  Errors: "auction: epsilon must be > 0",
+ * "auction: scale_factor must be > 1".  prices_out (n, nullable) receives
+ * the final prices; round_prices (round_cap x n, nullable) the price vector
+ * after each of the first round_cap rounds (the on_round observer). */
+typedef struct {
+  double epsilon;
+  int32_t has_epsilon;
+  int32_t scaling;
+  double scale_factor; /* 4.0 in AuctionConfig */
+  int64_t deadline_ns;
+} lsapgpu_auction_params;
+typedef struct {
+  int64_t outer_iterations;   /* SolveReport::outer_iterations (bidding rounds) */
+  int64_t switches_applied;   /* awards, displacements included */
+  int32_t terminated_by;      /* 0 converged, 1 deadline */
+  int32_t completed_greedily; /* SolveReport::completed_greedily */
+  double value;               /* ordered objective of the final assignment */
+  double elapsed_ms;
+  /* instrumentation */
+  int64_t bids;               /* agent row scans */
+  int64_t phases;             /* epsilon phases run */
+  double epsilon;             /* the target epsilon */
+  int64_t bytes_scanned;      /* bids * n * (storage element + fp64 price) */
+  int32_t storage;
+  int32_t pad_;
+} lsapgpu_auction_stats;
+int lsapgpu_auction_solve(lsapgpu_ctx* ctx, const lsapgpu_auction_params* params, int32_t* sigma_out,
+                          int32_t* tau_out, lsapgpu_auction_stats* stats, double* prices_out,
+                          double* round_prices, int64_t round_cap);
 
 /* Host helpers (sequential by nature; identical to the reference's). */
 void lsapgpu_random_perm(int32_t n, uint64_t seed, int32_t* out);

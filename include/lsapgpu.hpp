@@ -10,6 +10,10 @@
 //   lsap::gpu::evaluate_all_parallel     <- lsap::evaluate_all_parallel     (parallel.hpp:60-61)
 //   lsap::gpu::check_conflicts           <- lsap::check_conflicts           (parallel.hpp:65)
 //   lsap::gpu::apply_parallel_switches   <- lsap::apply_parallel_switches   (parallel.hpp:71-74)
+//   lsap::gpu::auction_solve             <- lsap::auction_solve             (baselines.hpp:33-36)
+//
+// auction_solve additionally needs lsap/baselines.hpp (AuctionConfig) included
+// before this header; define LSAPGPU_NO_AUCTION to leave it out.
 //
 // Same argument meaning, same results (bit for bit), same lsap::Error messages;
 // `workers` / `chunk` are validated and otherwise ignored (the reference's
@@ -17,7 +21,9 @@
 // context caches device memory and the CUDA graph between calls.
 #pragma once
 
+#include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -192,5 +198,58 @@ inline std::pair<Assignment, std::vector<AppliedExchange>> apply_parallel_switch
   for (std::int32_t q = 0; q < k; ++q) applied[q] = {a1[q], a2[q], a3[q], a4[q], a5[q]};
   return {std::move(out), std::move(applied)};
 }
+
+#ifndef LSAPGPU_NO_AUCTION
+// lsap::auction_solve (auction.cpp:110-153) on the device.  on_round, when
+// set, observes the price vector after every round: the rounds are recorded
+// on the device (up to `round_cap`, the run repeated with an exact buffer when
+// longer and no deadline is set) and replayed to the observer in order.
+inline SolveReport auction_solve(const Instance& inst, const AuctionConfig& cfg = {},
+                                 const std::function<void(const std::vector<double>&)>& on_round = {},
+                                 int device = 0, std::int64_t round_cap = 4096) {
+  inst.validate();
+  cfg.validate();
+  Context& ctx = context(device);
+  ctx.set_instance(inst);
+  lsapgpu_auction_params p{};
+  p.has_epsilon = cfg.epsilon ? 1 : 0;
+  p.epsilon = cfg.epsilon ? *cfg.epsilon : 0.0;
+  p.scaling = cfg.scaling ? 1 : 0;
+  p.scale_factor = cfg.scale_factor;
+  p.deadline_ns = cfg.deadline ? static_cast<std::int64_t>(cfg.deadline->count()) : -1;
+  const std::int32_t n = inst.n;
+  SolveReport rep;
+  rep.assignment.sigma.resize(n);
+  rep.assignment.tau.resize(n);
+  lsapgpu_auction_stats st{};
+  std::int64_t cap = on_round ? round_cap : 0;
+  std::vector<double> rounds;
+  auto run = [&]() {
+    rounds.assign(static_cast<std::size_t>(cap) * n, 0.0);
+    ctx.check(lsapgpu_auction_solve(ctx.get(), &p, rep.assignment.sigma.data(), rep.assignment.tau.data(), &st,
+                                    nullptr, cap ? rounds.data() : nullptr, cap));
+  };
+  run();
+  if (on_round && st.outer_iterations > cap && !cfg.deadline) {
+    cap = st.outer_iterations;
+    run();
+  }
+  if (on_round) {
+    std::vector<double> prices(static_cast<std::size_t>(n));
+    for (std::int64_t r = 0; r < cap && r < st.outer_iterations; ++r) {
+      std::copy(rounds.begin() + r * n, rounds.begin() + (r + 1) * n, prices.begin());
+      on_round(prices);
+    }
+  }
+  rep.assignment.value = st.value;
+  rep.outer_iterations = st.outer_iterations;
+  rep.switches_applied = st.switches_applied;
+  rep.terminated_by = st.terminated_by ? Termination::deadline : Termination::converged;
+  rep.completed_greedily = st.completed_greedily != 0;
+  rep.objective_trace.emplace_back(0, rep.assignment.value);  // auction.cpp:149
+  rep.elapsed = std::chrono::duration_cast<Duration>(std::chrono::duration<double, std::milli>(st.elapsed_ms));
+  return rep;
+}
+#endif
 
 }  // namespace lsap::gpu

@@ -682,3 +682,133 @@ done:
   state_free(&st);
   return rc;
 }
+
+/* ==== auction.cpp: synchronous (Jacobi) auction ============================ */
+
+/* net_scan contract (kernels_scalar.cpp:40-54): max over k != skip of
+ * row[k] - prices[k], first k on ties. */
+static double orc_net_scan(const double* row, const double* prices, int32_t n, int32_t skip,
+                           int32_t* best_k_out) {
+  int32_t best_k = -1;
+  double best = 0.0;
+  for (int32_t k = 0; k < n; ++k) {
+    if (k == skip) continue;
+    const double d = row[k] - prices[k];
+    if (best_k < 0 || d > best) {
+      best = d;
+      best_k = k;
+    }
+  }
+  if (best_k_out) *best_k_out = best_k;
+  return best_k < 0 ? 0.0 : best;
+}
+
+/* run_phase (auction.cpp:33-80); returns 0 when the deadline fired */
+static int orc_auction_phase(const double* a, int32_t n, double* prices, int32_t* owner,
+                             int32_t* assigned, int32_t* unassigned, double eps,
+                             int64_t expire_round, int64_t* checks, orc_auction_stats* S,
+                             double* bid_value, int32_t* bid_winner) {
+  while (*unassigned > 0) {
+    if (expire_round >= 0 && (*checks)++ >= expire_round) return 0;
+    S->rounds++;
+    for (int32_t j = 0; j < n; ++j) {
+      bid_value[j] = -INFINITY;
+      bid_winner[j] = -1;
+    }
+    for (int32_t i = 0; i < n; ++i) {
+      if (assigned[i] >= 0) continue;
+      const double* row = a + (size_t)i * n;
+      int32_t bk = -1;
+      const double best = orc_net_scan(row, prices, n, -1, &bk);
+      const double second = n > 1 ? orc_net_scan(row, prices, n, bk, NULL) : best;
+      const double bid = prices[bk] + (best - second) + eps;
+      S->bids++;
+      if (bid > bid_value[bk]) {  /* ascending i: ties go to the smallest agent */
+        bid_value[bk] = bid;
+        bid_winner[bk] = i;
+      }
+    }
+    for (int32_t j = 0; j < n; ++j) {
+      const int32_t w = bid_winner[j];
+      if (w < 0) continue;
+      const int32_t prev = owner[j];
+      if (prev >= 0) {
+        assigned[prev] = -1;
+        ++*unassigned;
+      }
+      owner[j] = w;
+      assigned[w] = j;
+      --*unassigned;
+      prices[j] = bid_value[j];
+      S->switches++;
+    }
+  }
+  return 1;
+}
+
+int orc_auction_solve(const double* a, int32_t n, int has_eps, double eps, int scaling,
+                      double scale_factor, int64_t expire_round, int32_t* sigma_out,
+                      double* prices_out, orc_auction_stats* stats) {
+  orc_auction_stats S;
+  memset(&S, 0, sizeof(S));
+  if (n < 1 || orc_validate(a, n) != 0) return 1;
+  if (has_eps && !(eps > 0.0)) return 1;        /* "auction: epsilon must be > 0" */
+  if (!(scale_factor > 1.0)) return 1;          /* "auction: scale_factor must be > 1" */
+  const size_t N = (size_t)n;
+  double lo = a[0], hi = a[0];
+  for (size_t k = 1; k < N * N; ++k) {          /* std::minmax_element (auction.cpp:116) */
+    if (a[k] < lo) lo = a[k];
+    if (!(a[k] < hi)) hi = a[k];
+  }
+  const double range = hi - lo;
+  const double eps_target = has_eps ? eps : (range > 0.0 ? range / (2.0 * n) : 1.0);
+  S.epsilon = eps_target;
+  double* prices = (double*)calloc(N, sizeof(double));
+  int32_t* owner = (int32_t*)malloc(N * sizeof(int32_t));
+  int32_t* assigned = (int32_t*)malloc(N * sizeof(int32_t));
+  double* bid_value = (double*)malloc(N * sizeof(double));
+  int32_t* bid_winner = (int32_t*)malloc(N * sizeof(int32_t));
+  int32_t unassigned = n;
+  int64_t checks = 0;
+  int finished = 1;
+  double e = scaling ? (range > 0.0 ? range / 2.0 : eps_target) : eps_target;
+  if (e < eps_target) e = eps_target;
+  for (;;) {
+    for (int32_t x = 0; x < n; ++x) owner[x] = assigned[x] = -1;  /* clear_assignment */
+    unassigned = n;
+    finished = orc_auction_phase(a, n, prices, owner, assigned, &unassigned, e, expire_round, &checks,
+                                 &S, bid_value, bid_winner);
+    if (!scaling || !finished || e <= eps_target) break;
+    e = e / scale_factor;
+    if (e < eps_target) e = eps_target;
+  }
+  if (!finished) {  /* complete_greedily (auction.cpp:84-106) */
+    for (int32_t i = 0; i < n; ++i) {
+      if (assigned[i] >= 0) continue;
+      int32_t bj = -1;
+      double best = -INFINITY;
+      for (int32_t j = 0; j < n; ++j) {  /* free jobs in ascending order */
+        if (owner[j] >= 0) continue;
+        const double v = a[(size_t)i * n + j];
+        if (v > best) {
+          best = v;
+          bj = j;
+        }
+      }
+      owner[bj] = i;
+      assigned[i] = bj;
+    }
+    S.terminated_by = 1;
+    S.completed_greedily = 1;
+  }
+  memcpy(sigma_out, owner, N * sizeof(int32_t));
+  S.value = orc_objective(a, n, owner);
+  if (prices_out) memcpy(prices_out, prices, N * sizeof(double));
+  if (stats) *stats = S;
+  free(prices);
+  free(owner);
+  free(assigned);
+  free(bid_value);
+  free(bid_winner);
+  return 0;
+}

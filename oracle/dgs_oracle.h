@@ -109,6 +109,25 @@ int orc_dgs_parallel(const double* a, int32_t n, uint64_t seed, double eps, int 
                      orc_stats* stats, int64_t* trace_switch, double* trace_value,
                      int64_t trace_cap, int64_t* trace_len);
 
+/* ---- auction.cpp:12-153: the synchronous auction baseline ------------------
+ * AuctionConfig (baselines.hpp:12-26): has_eps selects epsilon; scaling and
+ * scale_factor as there.  expire_round < 0: no deadline; k >= 0: the deadline
+ * check (auction.cpp:42) fires at the (k+1)-th check, so 0 reproduces
+ * deadline = 0 deterministically.  prices_out (nullable) receives the final
+ * prices.  Returns 0, or 1 on a config error (the reference's messages). */
+typedef struct {
+  int64_t rounds;      /* SolveReport::outer_iterations */
+  int64_t switches;    /* awards, displacements included */
+  int64_t bids;        /* agent row scans (two net_scans each) */
+  int32_t terminated_by;
+  int32_t completed_greedily;
+  double value;
+  double epsilon;      /* target epsilon */
+} orc_auction_stats;
+int orc_auction_solve(const double* a, int32_t n, int has_eps, double eps, int scaling,
+                      double scale_factor, int64_t expire_round, int32_t* sigma_out,
+                      double* prices_out, orc_auction_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

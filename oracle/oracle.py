@@ -56,6 +56,27 @@ class _Stats(C.Structure):
     ]
 
 
+class _AuctionStats(C.Structure):
+    _fields_ = [("rounds", C.c_int64), ("switches", C.c_int64), ("bids", C.c_int64),
+                ("terminated_by", C.c_int32), ("completed_greedily", C.c_int32),
+                ("value", C.c_double), ("epsilon", C.c_double)]
+
+
+@dataclass
+class AuctionResult:
+    sigma: np.ndarray
+    value: float
+    rounds: int
+    switches: int
+    terminated_by: str
+    completed_greedily: bool
+    prices: np.ndarray
+    elapsed_ms: float = -1.0
+    bids: int = -1
+    monotone: bool = True
+    round_count: int = -1
+
+
 def _as(a, dt):
     return np.ascontiguousarray(a, dtype=dt)
 
@@ -89,6 +110,8 @@ class Oracle:
             _dp, C.c_int32, _ip, _ip, C.POINTER(C.c_double), _dp, _ip, _bp, _dp, _ip, _bp, _bp, _bp,
             C.c_double, _ip, _ip, _ip, _ip, _dp]
         L.orc_dgs_parallel.restype = C.c_int
+        L.orc_auction_solve.argtypes = [_dp, C.c_int32, C.c_int, C.c_double, C.c_int, C.c_double,
+                                        C.c_int64, _ip, _dp, C.POINTER(_AuctionStats)]
         L.orc_dgs_parallel.argtypes = [
             _dp, C.c_int32, C.c_uint64, C.c_double, C.c_int, C.c_int64, C.c_int, _ip, _ip,
             C.POINTER(_Stats), _lp, _dp, C.c_int64, C.POINTER(C.c_int64)]
@@ -189,6 +212,22 @@ class Oracle:
                            "deadline" if st.terminated_by else "converged", st.elapsed_ms, tr,
                            st.inner_iterations, st.agent_scans, st.job_scans, st.pair_items)
 
+    def auction_solve(self, a, epsilon=None, scaling=False, scale_factor=4.0,
+                      expire_round: int = -1) -> AuctionResult:
+        """auction.cpp restatement; expire_round = k fires the deadline at the
+        (k+1)-th round check (0 = the reference's deadline 0)."""
+        a = _as(a, np.float64)
+        n = a.shape[0]
+        sig, pr = np.empty(n, np.int32), np.empty(n)
+        st = _AuctionStats()
+        if self.lib.orc_auction_solve(a.ravel(), n, 0 if epsilon is None else 1,
+                                      0.0 if epsilon is None else float(epsilon), 1 if scaling else 0,
+                                      float(scale_factor), expire_round, sig, pr, C.byref(st)):
+            raise ValueError("invalid auction instance / config")
+        return AuctionResult(sig, st.value, st.rounds, st.switches,
+                             "deadline" if st.terminated_by else "converged", bool(st.completed_greedily),
+                             pr, bids=st.bids)
+
 
 class RefLib:
     """The unmodified reference library (oracle/_ref/liblsap_ref.so)."""
@@ -206,6 +245,10 @@ class RefLib:
             _dp, C.c_int32, C.c_uint64, C.c_double, C.c_int, C.c_int64, C.c_int, _ip, _ip,
             C.POINTER(C.c_double), i64p, i64p, C.POINTER(C.c_int), C.POINTER(C.c_double),
             _lp, _dp, C.c_int64, i64p]
+        L.ref_auction_solve.argtypes = [_dp, C.c_int32, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int64,
+                                        _ip, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_double), _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
         L.ref_evaluate_all.argtypes = [_dp, C.c_int32, _ip, C.c_double, C.c_int, _dp, _ip, _dp, _ip]
         L.ref_check_conflicts.argtypes = [C.c_int32, _dp, _ip, C.c_void_p, _dp, _ip, C.c_void_p, _ip,
                                           _bp, _bp, _bp, _bp, _ip, C.POINTER(C.c_int32)]
@@ -287,6 +330,26 @@ class RefLib:
         tr = [(int(ts[k]), float(tv[k])) for k in range(min(tl.value, cap))] if trace else []
         return SolveResult(sig, tau, val.value, outer.value, sw.value,
                            "deadline" if term.value else "converged", el.value, tr)
+
+    def auction_solve(self, a, epsilon=None, scaling=False, scale_factor=4.0,
+                      deadline_ns: int = -1) -> AuctionResult:
+        """lsap::auction_solve (auction.cpp:110-153), with an on_round observer
+        recording the last price vector, the round count and monotonicity."""
+        a = _as(a, np.float64)
+        n = a.shape[0]
+        sig, pr = np.empty(n, np.int32), np.empty(n)
+        val, el = C.c_double(), C.c_double()
+        outer, sw, rounds = C.c_int64(), C.c_int64(), C.c_int64()
+        term, greedy, mono = C.c_int(), C.c_int(), C.c_int()
+        if self.lib.ref_auction_solve(a.ravel(), n, 0 if epsilon is None else 1,
+                                      0.0 if epsilon is None else float(epsilon), 1 if scaling else 0,
+                                      float(scale_factor), deadline_ns, sig, C.byref(val), C.byref(outer),
+                                      C.byref(sw), C.byref(term), C.byref(greedy), C.byref(el), pr,
+                                      C.byref(rounds), C.byref(mono)):
+            raise ValueError(self._err())
+        return AuctionResult(sig, val.value, outer.value, sw.value,
+                             "deadline" if term.value else "converged", bool(greedy.value), pr,
+                             elapsed_ms=el.value, monotone=bool(mono.value), round_count=rounds.value)
 
 
 def load_ref_or_none():

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "lsap/baselines.hpp"
 #include "lsap/core.hpp"
 #include "lsap/dgs.hpp"
 #include "lsap/geom.hpp"
@@ -188,6 +189,51 @@ std::int32_t ref_apply_parallel_switches(
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;
+  }
+}
+
+// lsap::auction_solve (auction.cpp:110-153).  has_eps selects
+// AuctionConfig::epsilon; prices_out (nullable) receives the price vector the
+// on_round observer saw last; rounds_out the number of observed rounds and
+// monotone_out whether prices never decreased between rounds
+// (test_baselines.cpp:104-115).
+int ref_auction_solve(const double* a, std::int32_t n, int has_eps, double eps, int scaling,
+                      double scale_factor, std::int64_t deadline_ns, std::int32_t* sigma_out,
+                      double* value_out, std::int64_t* outer_out, std::int64_t* switches_out,
+                      int* terminated_out, int* greedy_out, double* elapsed_ms_out,
+                      double* prices_out, std::int64_t* rounds_out, int* monotone_out) {
+  try {
+    const auto inst = make_instance(a, n);
+    lsap::AuctionConfig cfg;
+    if (has_eps) cfg.epsilon = eps;
+    cfg.scaling = scaling != 0;
+    cfg.scale_factor = scale_factor;
+    if (deadline_ns >= 0) cfg.deadline = lsap::Duration{deadline_ns};
+    std::vector<double> last;
+    std::int64_t rounds = 0;
+    bool monotone = true;
+    const auto rep = lsap::auction_solve(inst, cfg, [&](const std::vector<double>& prices) {
+      if (!last.empty())
+        for (std::size_t j = 0; j < prices.size(); ++j) monotone &= prices[j] >= last[j];
+      last = prices;
+      ++rounds;
+    });
+    std::memcpy(sigma_out, rep.assignment.sigma.data(), sizeof(std::int32_t) * n);
+    *value_out = rep.assignment.value;
+    *outer_out = rep.outer_iterations;
+    *switches_out = rep.switches_applied;
+    *terminated_out = rep.terminated_by == lsap::Termination::deadline ? 1 : 0;
+    *greedy_out = rep.completed_greedily ? 1 : 0;
+    *elapsed_ms_out = std::chrono::duration<double, std::milli>(rep.elapsed).count();
+    if (prices_out) {
+      if (last.empty()) last.assign(static_cast<std::size_t>(n), 0.0);
+      std::memcpy(prices_out, last.data(), sizeof(double) * n);
+    }
+    if (rounds_out) *rounds_out = rounds;
+    if (monotone_out) *monotone_out = monotone ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
   }
 }
 

@@ -7,6 +7,7 @@ mirror of the reference's data types and entry points in :mod:`.lsap`.
 from .lsap import (  # noqa: F401
     AppliedExchange,
     Assignment,
+    AuctionConfig,
     ConflictSets,
     Context,
     DeltaTables,
@@ -18,6 +19,7 @@ from .lsap import (  # noqa: F401
     SolveReport,
     agent_exchange_delta,
     apply_parallel_switches,
+    auction_solve,
     check_conflicts,
     context,
     dgs_parallel,

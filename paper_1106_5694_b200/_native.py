@@ -27,7 +27,7 @@ EXPORTS = [
     "lsapgpu_evaluate_all", "lsapgpu_check_conflicts", "lsapgpu_apply_parallel_switches",
     "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_solve_dist",
     "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
-    "lsapgpu_set_timeline", "lsapgpu_timeline",
+    "lsapgpu_set_timeline", "lsapgpu_timeline", "lsapgpu_auction_solve",
 ]
 
 
@@ -55,6 +55,36 @@ class Stats(C.Structure):
         ("job_scans", C.c_int64),
         ("lfmm_rounds", C.c_int64),
         ("scan_launches", C.c_int64),
+        ("bytes_scanned", C.c_int64),
+        ("storage", C.c_int32),
+        ("pad_", C.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+class AuctionParams(C.Structure):
+    _fields_ = [
+        ("epsilon", C.c_double),
+        ("has_epsilon", C.c_int32),
+        ("scaling", C.c_int32),
+        ("scale_factor", C.c_double),
+        ("deadline_ns", C.c_int64),
+    ]
+
+
+class AuctionStats(C.Structure):
+    _fields_ = [
+        ("outer_iterations", C.c_int64),
+        ("switches_applied", C.c_int64),
+        ("terminated_by", C.c_int32),
+        ("completed_greedily", C.c_int32),
+        ("value", C.c_double),
+        ("elapsed_ms", C.c_double),
+        ("bids", C.c_int64),
+        ("phases", C.c_int64),
+        ("epsilon", C.c_double),
         ("bytes_scanned", C.c_int64),
         ("storage", C.c_int32),
         ("pad_", C.c_int32),
@@ -115,6 +145,8 @@ def _load() -> C.CDLL:
         "lsapgpu_set_scan_timing": (C.c_int, [vp, C.c_int]),
         "lsapgpu_set_timeline": (C.c_int, [vp, C.c_int32]),
         "lsapgpu_timeline": (C.c_int32, [vp, C.c_void_p, C.c_int32]),
+        "lsapgpu_auction_solve": (C.c_int, [vp, C.POINTER(AuctionParams), vp, vp, C.POINTER(AuctionStats),
+                                            vp, vp, i64]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
                                           C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),
     }

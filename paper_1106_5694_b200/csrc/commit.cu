@@ -232,6 +232,7 @@ CommitPlan plan_commit(const DevState& d) {
   if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE"))
     if (std::atoi(s) == 0) p.cta_edge_cap = 0;
   if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE_MAX")) p.cta_edge_cap = std::min(p.cta_edge_cap, std::atoi(s));
+  if (const char* s = std::getenv("LSAPGPU_COMMIT_VARIANT")) p.variant = std::atoi(s);
   return p;
 }
 

@@ -76,7 +76,7 @@ struct EdgeArrays {
 template <class E, int CS>
 __global__ void __launch_bounds__(kNT, 1)
     commit_cluster_kernel(DevState st, int mode, cudaGraphConditionalHandle cond, int use_cond,
-                          int edge_cap, int cta_cap) {
+                          int edge_cap, int cta_cap, int var) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x;
@@ -229,17 +229,22 @@ __global__ void __launch_bounds__(kNT, 1)
       const int32_t u = Ea.u[l], v = Ea.v[l];
       uint32_t* ku = kbase[u % CS] + u / CS;
       uint32_t* kv = kbase[v % CS] + v / CS;
-      if (rounds > 0 && (*ku == kMatched || *kv == kMatched)) {  // nothing is matched in round 1
+      const bool pre = rounds > 0 || (var & 1);  // nothing is matched in round 1
+      const uint32_t cu = pre ? *ku : 0u, cv = pre ? *kv : 0u;
+      if (cu == kMatched || cv == kMatched) {
         Ea.st[l] = kEdgeRejected;
       } else {
+        // keys only grow within a round: skip the (serialising, remote)
+        // atomic when a higher priority is already posted
         const uint32_t k = make_key(R, Ea.slot[l]);
-        atomicMax(ku, k);
-        atomicMax(kv, k);
+        if (cu < k) atomicMax(ku, k);
+        if (cv < k) atomicMax(kv, k);
         ++local;
       }
     }
     block_add(local, &sc.count[rounds & 1]);
     cluster.sync();
+    if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 13);
     if (tid == 0) {
       int tot = 0;
 #pragma unroll
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(kNT, 1)
       }
     }
     cluster.sync();  // bitmap and committed list complete
+    if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 14);
     for (int32_t base = tid - lane; base < cnt; base += kNT) {
       const int32_t l = base + lane;
       bool q = false;
@@ -495,7 +501,7 @@ cudaError_t launch_cs(const DevState& d, const CommitPlan& p, int mode, cudaGrap
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = d.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap);
+  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap, p.variant);
 }
 
 template <int CS>

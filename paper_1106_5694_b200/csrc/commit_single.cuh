@@ -110,12 +110,13 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
     for (int32_t l = tid; l < m; l += kNT) {
       if (Est[l] != kEdgeUndecided) continue;
       const int32_t u = Ea[l], v = Ed[l];
-      if (keys[u] == kMatched || keys[v] == kMatched) {
+      const uint32_t cu = keys[u], cv = keys[v];
+      if (cu == kMatched || cv == kMatched) {
         Est[l] = kEdgeRejected;
       } else {
-        const uint32_t k = make_key(R, Eslot[l]);
-        atomicMax(&keys[u], k);
-        atomicMax(&keys[v], k);
+        const uint32_t k = make_key(R, Eslot[l]);  // keys only grow within a round
+        if (cu < k) atomicMax(&keys[u], k);
+        if (cv < k) atomicMax(&keys[v], k);
         local = 1;
       }
     }

@@ -190,6 +190,16 @@ struct lsapgpu_ctx {
   void* ring[kRing] = {};         // pinned bounce buffers
   size_t ring_bytes = 0;
   HostPool* pool = nullptr;
+
+  // auction baseline (auction.cu): per-n vectors (in vec_bufs), the epsilon
+  // schedule and the benefit range of the current matrix
+  AuctionDev au;
+  int32_t au_n = 0;
+  AuctionCtrl* au_host = nullptr;  // pinned
+  double* eps_dev = nullptr;
+  size_t eps_cap = 0;
+  bool range_ok = false;
+  double lo = 0.0, hi = 0.0;
 };
 
 namespace {
@@ -224,6 +234,7 @@ void free_vectors(lsapgpu_ctx* ctx) {
   for (auto& b : ctx->vec_bufs) cudaFree(b.p);
   ctx->vec_bufs.clear();
   ctx->n_vec = 0;
+  ctx->au_n = 0;
 }
 
 template <class T>
@@ -341,6 +352,7 @@ void finish_matrix(lsapgpu_ctx* ctx, int32_t n) {
   ctx->scan_plan = plan_scan(ctx->d, ctx->num_sms);
   ctx->commit_plan = plan_commit(ctx->d);
   ctx->n_matrix = n;
+  ctx->range_ok = false;
 }
 
 // Builds A/AT from a layout source; src_rows_dev is a device pointer for memory sources.
@@ -704,6 +716,8 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->d.tl) cudaFree(ctx->d.tl);
   if (ctx->obj_pin) cudaFreeHost(ctx->obj_pin);
+  if (ctx->au_host) cudaFreeHost(ctx->au_host);
+  if (ctx->eps_dev) cudaFree(ctx->eps_dev);
   if (ctx->log_pin) cudaFreeHost(ctx->log_pin);
   if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   if (ctx->stage.p) cudaFree(ctx->stage.p);
@@ -1292,3 +1306,132 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
 }
 
 }  // extern "C"
+
+// ---- auction baseline: lsap::auction_solve (auction.cpp:110-153) ----------
+
+int lsapgpu_auction_solve(lsapgpu_ctx* ctx, const lsapgpu_auction_params* params, int32_t* sigma_out,
+                          int32_t* tau_out, lsapgpu_auction_stats* stats, double* prices_out,
+                          double* round_prices, int64_t round_cap) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (!ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  if (!params || !sigma_out) return fail(ctx, LSAPGPU_ERR_INVALID, "null argument");
+  const lsapgpu_auction_params& P = *params;
+  // AuctionConfig::validate (baselines.hpp:22-25)
+  if (P.has_epsilon && !(P.epsilon > 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "auction: epsilon must be > 0");
+  if (!(P.scale_factor > 1.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "auction: scale_factor must be > 1");
+  if (round_cap < 0 || (round_cap > 0 && !round_prices))
+    return fail(ctx, LSAPGPU_ERR_INVALID, "round_prices needs round_cap entries");
+  CK(cudaSetDevice(ctx->device));
+  const auto t_start = std::chrono::steady_clock::now();
+  auto elapsed_ns = [&]() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_start)
+        .count();
+  };
+  const int32_t n = ctx->n_matrix;
+  DevState& d = ctx->d;
+  AuctionDev& a = ctx->au;
+  if (!ctx->au_host) CK(cudaMallocHost(&ctx->au_host, sizeof(AuctionCtrl)));
+  if (ctx->au_n != n) {
+    const size_t N = static_cast<size_t>(d.ld), NC = N * 16;  // segments for up to 16 cluster CTAs
+    CK(valloc(ctx, &a.prices, N, false));
+    CK(valloc(ctx, &a.owner, N, false));
+    CK(valloc(ctx, &a.assigned, N, false));
+    CK(valloc(ctx, &a.slot, 2 * N, false));
+    CK(valloc(ctx, &a.rec_i, NC, false));
+    CK(valloc(ctx, &a.rec_j, NC, false));
+    CK(valloc(ctx, &a.rec_bid, NC, false));
+    CK(valloc(ctx, &a.wl[0], NC, false));
+    CK(valloc(ctx, &a.wl[1], NC, false));
+    CK(valloc(ctx, &a.ctrl, 1, false));
+    ctx->au_n = n;
+  }
+  a.local_prices = n <= auction_local_price_cap() ? 1 : 0;
+  if (const char* e = std::getenv("LSAPGPU_AUCTION_LOCAL_PRICES")) a.local_prices = a.local_prices && std::atoi(e);
+  AuctionCtrl& H = *ctx->au_host;
+
+  // benefit range (std::minmax_element, auction.cpp:116-117), once per matrix
+  if (!ctx->range_ok) {
+    std::memset(&H, 0, sizeof(H));
+    H.lo_key = ~0ull;
+    CK(cpy(ctx, a.ctrl, &H, sizeof(H), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_minmax(d, a.ctrl, ctx->stream));
+    ++ctx->launches;
+    CK(cpy(ctx, &H, a.ctrl, sizeof(H), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->lo = auction_key_value(H.lo_key);
+    ctx->hi = auction_key_value(H.hi_key);
+    ctx->range_ok = true;
+  }
+  const double range = ctx->hi - ctx->lo;
+  const double eps_target = P.has_epsilon ? P.epsilon : (range > 0.0 ? range / (2.0 * n) : 1.0);
+  // the epsilon schedule (auction.cpp:125-135)
+  std::vector<double> eps_list;
+  if (P.scaling) {
+    double eps = std::max(eps_target, range > 0.0 ? range / 2.0 : eps_target);
+    while (true) {
+      eps_list.push_back(eps);
+      if (eps <= eps_target) break;
+      eps = std::max(eps_target, eps / P.scale_factor);
+    }
+  } else {
+    eps_list.push_back(eps_target);
+  }
+  if (ctx->eps_cap < eps_list.size()) {
+    if (ctx->eps_dev) cudaFree(ctx->eps_dev);
+    ctx->eps_dev = nullptr;
+    ctx->eps_cap = 0;
+    CK(cudaMalloc(&ctx->eps_dev, sizeof(double) * eps_list.size()));
+    ctx->eps_cap = eps_list.size();
+  }
+  CK(cpy(ctx, ctx->eps_dev, eps_list.data(), sizeof(double) * eps_list.size(), cudaMemcpyHostToDevice,
+         ctx->stream));
+  a.eps_list = ctx->eps_dev;
+  a.n_eps = static_cast<int32_t>(eps_list.size());
+  double* rp_dev = nullptr;
+  if (round_cap > 0) CK(cudaMallocAsync(&rp_dev, sizeof(double) * round_cap * n, ctx->stream));
+  a.round_prices = rp_dev;
+  a.round_cap = round_cap;
+
+  const size_t N = static_cast<size_t>(d.ld);
+  CK(cudaMemsetAsync(a.prices, 0, sizeof(double) * N, ctx->stream));
+  CK(cudaMemsetAsync(a.slot, 0, sizeof(unsigned long long) * 2 * N, ctx->stream));
+  const unsigned long long lo_key = H.lo_key, hi_key = H.hi_key;
+  std::memset(&H, 0, sizeof(H));
+  H.lo_key = lo_key;
+  H.hi_key = hi_key;
+  CK(cpy(ctx, a.ctrl, &H, sizeof(H), cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t remaining = P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns());
+  CK(launch_auction(d, a, remaining, ctx->stream));
+  ++ctx->launches;
+  // make_assignment (core.cpp:36-50): tau from sigma, ordered objective
+  CK(launch_init_assignment(d, ctx->stream));
+  ++ctx->launches;
+  int rc = enqueue_objective(ctx);
+  if (rc) return rc;
+  CK(cpy(ctx, &H, a.ctrl, sizeof(H), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tau_out) CK(cpy(ctx, tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (prices_out) CK(cpy(ctx, prices_out, a.prices, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rp_dev) {
+    CK(cpy(ctx, round_prices, rp_dev, sizeof(double) * round_cap * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaFreeAsync(rp_dev, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double value = objective_sum(ctx);
+  const double ms = static_cast<double>(elapsed_ns()) / 1e6;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->outer_iterations = H.rounds;
+    stats->switches_applied = H.switches;
+    stats->terminated_by = H.finished ? 0 : 1;
+    stats->completed_greedily = H.greedy;
+    stats->value = value;
+    stats->elapsed_ms = ms;
+    stats->bids = H.bids;
+    stats->phases = H.phases;
+    stats->epsilon = eps_target;
+    stats->bytes_scanned = H.bids * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage) + 8);
+    stats->storage = d.storage;
+  }
+  return LSAPGPU_OK;
+}

@@ -147,9 +147,11 @@ struct CommitPlan {
   size_t cluster_smem = 0;  // cluster kernel: dynamic smem per CTA
   int edge_cap = 0;         // cluster kernel: proposals per CTA held in smem
   int cta_edge_cap = 0;     // single-CTA path taken when the proposals fit one CTA (0: never)
+  int variant = 1;          // cluster kernel bit 0: read keys before the round-1 atomics
   bool operator==(const CommitPlan& o) const {
     return threads == o.threads && smem == o.smem && keys_in_smem == o.keys_in_smem && cluster == o.cluster &&
-           cluster_smem == o.cluster_smem && edge_cap == o.edge_cap && cta_edge_cap == o.cta_edge_cap;
+           cluster_smem == o.cluster_smem && edge_cap == o.edge_cap && cta_edge_cap == o.cta_edge_cap &&
+           variant == o.variant;
   }
 };
 CommitPlan plan_commit(const DevState& d);
@@ -163,5 +165,40 @@ cudaError_t launch_edges_from_tables(const DevState& d, cudaStream_t st);
 cudaError_t launch_tau16_sync(const DevState& d, cudaStream_t st);
 cudaError_t launch_accepted_from_masks(const DevState& d, const uint8_t* agent_acc,
                                        const uint8_t* job_acc, cudaStream_t st);
+
+// auction.cu (lsap::auction_solve, auction.cpp)
+struct AuctionCtrl {
+  int32_t count[2];  // bidder lists (ping-pong)
+  int32_t expired;   // deadline fired (decided by CTA 0 at round boundaries)
+  int32_t finished;  // every phase converged
+  int32_t greedy;    // completed greedily after a deadline
+  int32_t pad_;
+  int64_t rounds;    // SolveReport::outer_iterations
+  int64_t switches;  // awards, including displacements
+  int64_t bids;      // agent row scans
+  int64_t phases;    // epsilon phases started
+  unsigned long long lo_key, hi_key;  // benefit range (order-preserving keys)
+};
+struct AuctionDev {
+  double* prices = nullptr;
+  int32_t* owner = nullptr;     // job -> agent (-1 free)
+  int32_t* assigned = nullptr;  // agent -> job (-1 unassigned)
+  unsigned long long* slot = nullptr;  // per job: {inverted agent, bid key} of the round's best bid
+  int32_t* rec_i = nullptr;     // bid records beyond a CTA's shared-memory capacity (CS x n)
+  int32_t* rec_j = nullptr;
+  double* rec_bid = nullptr;
+  int32_t* wl[2] = {nullptr, nullptr};  // bidder lists, one n-entry segment per cluster CTA
+  int local_prices = 0;         // 1: every CTA holds a shared-memory replica of the prices
+  AuctionCtrl* ctrl = nullptr;
+  const double* eps_list = nullptr;  // epsilon of every phase (host-computed schedule)
+  int32_t n_eps = 0;
+  double* round_prices = nullptr;    // optional on_round snapshots, round_cap x n
+  int64_t round_cap = 0;
+};
+int auction_cluster_size();
+int32_t auction_local_price_cap();
+cudaError_t launch_auction(const DevState& d, const AuctionDev& a, int64_t remaining_ns, cudaStream_t st);
+cudaError_t launch_minmax(const DevState& d, AuctionCtrl* c, cudaStream_t st);
+double auction_key_value(unsigned long long key);
 
 }  // namespace lsapgpu

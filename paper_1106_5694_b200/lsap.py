@@ -166,6 +166,22 @@ class ParallelConfig:
 
 
 @dataclass
+class AuctionConfig:
+    """AuctionConfig (baselines.hpp:12-26)."""
+    epsilon: Optional[float] = None  # None: (max - min) / (2n), or 1.0 for a constant matrix
+    scaling: bool = False
+    scale_factor: float = 4.0
+    deadline: Optional[int] = None   # nanoseconds; None = no deadline
+    device: int = 0
+
+    def validate(self) -> None:
+        if self.epsilon is not None and not (self.epsilon > 0.0):
+            raise Error("auction: epsilon must be > 0")
+        if not (self.scale_factor > 1.0):
+            raise Error("auction: scale_factor must be > 1")
+
+
+@dataclass
 class ConflictSets:
     reserved: List[int]
     conflicted: List[int]
@@ -386,6 +402,54 @@ class Context:
         rep.gpu["trace_len"] = tl.value
         return rep
 
+    def auction_solve(self, cfg: Optional["AuctionConfig"] = None, on_round=None,
+                      round_cap: int = 4096) -> SolveReport:
+        """lsap::auction_solve (auction.cpp:110-153) on this context's matrix.
+        ``on_round`` observes the price vector after every round (the device
+        records up to ``round_cap`` rounds; without a deadline a longer run is
+        repeated with an exact-size buffer, the solve being deterministic)."""
+        cfg = cfg or AuctionConfig()
+        cfg.validate()
+        n = self.n
+        p = N.AuctionParams()
+        p.has_epsilon = 0 if cfg.epsilon is None else 1
+        p.epsilon = 0.0 if cfg.epsilon is None else float(cfg.epsilon)
+        p.scaling = 1 if cfg.scaling else 0
+        p.scale_factor = float(cfg.scale_factor)
+        p.deadline_ns = -1 if cfg.deadline is None else int(cfg.deadline)
+        sigma = np.empty(n, np.int32)
+        tau = np.empty(n, np.int32)
+        prices = np.empty(n)
+        st = N.AuctionStats()
+
+        def run(cap):
+            rp = np.empty((cap, n)) if cap else None
+            self._check(N.LIB.lsapgpu_auction_solve(self.h, C.byref(p), N.ptr(sigma), N.ptr(tau), C.byref(st),
+                                                    N.ptr(prices), N.ptr(rp) if cap else None, cap))
+            return rp
+
+        cap = round_cap if on_round is not None else 0
+        rp = run(cap)
+        if on_round is not None and st.outer_iterations > cap and cfg.deadline is None:
+            cap = int(st.outer_iterations)
+            rp = run(cap)
+        if on_round is not None:
+            for r in range(min(cap, st.outer_iterations)):
+                on_round(rp[r])
+        rep = SolveReport(
+            assignment=Assignment(sigma, tau, st.value),
+            objective_trace=[(0, st.value)],  # auction.cpp:149
+            outer_iterations=st.outer_iterations,
+            switches_applied=st.switches_applied,
+            elapsed=int(st.elapsed_ms * 1e6),
+            terminated_by="deadline" if st.terminated_by else "converged",
+            completed_greedily=bool(st.completed_greedily),
+        )
+        rep.gpu = st.as_dict()
+        rep.gpu["storage"] = N.STORAGE_NAMES[st.storage]
+        rep.gpu["prices"] = prices
+        return rep
+
     def evaluate_all(self, sigma, eps: float = 0.0) -> DeltaTables:
         sigma = np.ascontiguousarray(sigma, np.int32)
         n = self.n
@@ -505,6 +569,16 @@ def dgs_parallel(inst: Instance, cfg: Optional[ParallelConfig] = None) -> SolveR
     ctx = context(cfg.device)
     ctx.set_instance(inst)
     return ctx.solve(cfg)
+
+
+def auction_solve(inst: Instance, cfg: Optional[AuctionConfig] = None, on_round=None) -> SolveReport:
+    """lsap::auction_solve (baselines.hpp:33-36) on the B200."""
+    cfg = cfg or AuctionConfig()
+    inst.validate()
+    cfg.validate()
+    ctx = context(cfg.device)
+    ctx.set_instance(inst)
+    return ctx.auction_solve(cfg, on_round=on_round)
 
 
 def evaluate_all_parallel(inst: Instance, asg: Assignment, tables: DeltaTables,

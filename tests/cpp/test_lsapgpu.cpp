@@ -14,6 +14,7 @@
 #include <exception>
 #include <string>
 
+#include "lsap/baselines.hpp"
 #include "lsap/bench.hpp"
 #include "lsap/core.hpp"
 #include "lsap/dgs.hpp"
@@ -171,6 +172,49 @@ int main() {
       const auto cut = gpu::dgs_parallel(inst, c);
       CHECK(cut.terminated_by == Termination::deadline);
       validate_assignment(inst, cut.assignment);
+    }
+    // auction_solve, bit for bit (test_baselines.cpp:62-160 instances + C1/P2P)
+    {
+      auto auction_both = [](const Instance& inst, const AuctionConfig& cfg) {
+        std::vector<std::vector<double>> rr, rg;
+        const auto ref = auction_solve(inst, cfg, [&](const std::vector<double>& p) { rr.push_back(p); });
+        const auto got = gpu::auction_solve(inst, cfg, [&](const std::vector<double>& p) { rg.push_back(p); });
+        CHECK(ref.assignment.sigma == got.assignment.sigma && ref.assignment.tau == got.assignment.tau);
+        CHECK(std::memcmp(&ref.assignment.value, &got.assignment.value, 8) == 0);
+        CHECK(ref.outer_iterations == got.outer_iterations && ref.switches_applied == got.switches_applied);
+        CHECK(ref.terminated_by == got.terminated_by && ref.completed_greedily == got.completed_greedily);
+        CHECK(rr == rg);  // every round's price vector
+      };
+      AuctionConfig c;
+      c.epsilon = 0.1;
+      auction_both(Instance(2, {0, 10, 10, 0}), c);
+      auction_both(Instance(1, {4.2}), {});
+      auction_both(generate_geom({24, 100.0, 17}), {});
+      AuctionConfig sc;
+      sc.scaling = true;
+      auction_both(generate_geom({48, 100.0, 23}), sc);
+      auction_both(generate_geom({128, 100.0, 31}), {});
+      auction_both(random_int_instance(1000, 0, 1000), {});
+      for (std::uint64_t seed = 0; seed < 12; ++seed) {
+        const std::int32_t n = 2 + static_cast<std::int32_t>(seed % 6);
+        AuctionConfig e;
+        e.epsilon = 0.9 / n;
+        auction_both(random_int_instance(n, 4000 + seed, 50), e);
+      }
+      AuctionConfig d;
+      d.deadline = Duration{0};
+      const Instance g256 = generate_geom({256, 100.0, 5});
+      const auto ref = auction_solve(g256, d);
+      const auto got = gpu::auction_solve(g256, d);
+      CHECK(got.terminated_by == Termination::deadline && got.completed_greedily);
+      CHECK(ref.assignment.sigma == got.assignment.sigma);
+      validate_assignment(g256, got.assignment);
+      AuctionConfig bad;
+      bad.epsilon = 0.0;
+      std::string ref_msg, gpu_msg;
+      try { auction_solve(g256, bad); } catch (const Error& e) { ref_msg = e.what(); }
+      try { gpu::auction_solve(g256, bad); } catch (const Error& e) { gpu_msg = e.what(); }
+      CHECK(!ref_msg.empty() && ref_msg == gpu_msg);
     }
   } catch (const std::exception& e) {
     std::fprintf(stderr, "exception: %s\n", e.what());

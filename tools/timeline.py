@@ -18,7 +18,7 @@ ctx.generate(a.kind, a.n, 0)
 ctx.set_timeline(8192)
 names = {1: "full_sweep", 2: "scan", 3: "commit:start", 4: "commit:end", 5: "single:loaded",
          6: "single:round_end", 7: "res:tau16", 8: "res:acur", 9: "res:stage0", 10: "res:cta0_done",
-         11: "cl:P1done", 12: "cl:round_end", 13: "cl:P3done", 14: "cl:P4done", 15: "apply"}
+         11: "cl:P1done", 12: "cl:round_end", 13: "cl:phaseA", 14: "cl:classified", 15: "apply"}
 for k in range(a.solves):
     ctx.timeline()  # clear
     r = ctx.solve(g.ParallelConfig(seed=0), trace=False)
