@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kNT, 1) auction_kernel(DevState st, AuctionDev
       }
       __syncthreads();
       const int32_t cnt = s_pre[CS];
+      if (rank == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 1);
       if (cnt == 0) break;
       if (s_expired) {
         finished = false;
@@ -235,6 +236,8 @@ __global__ void __launch_bounds__(kNT, 1) auction_kernel(DevState st, AuctionDev
           int sg = 0;
           while (s_pre[sg + 1] <= k) ++sg;
           i = ldcg(wl + static_cast<int64_t>(sg) * n + (k - s_pre[sg]));
+          // lane-consecutive elements: coalesced row loads, conflict-free
+          // price reads (a 16-byte-vector variant measured slower)
           const E* row = A + static_cast<int64_t>(i) * ld;
           if (sprice) {
 #pragma unroll 4
@@ -270,7 +273,9 @@ __global__ void __launch_bounds__(kNT, 1) auction_kernel(DevState st, AuctionDev
         }
         __syncthreads();
       }
+      if (rank == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 2);
       cluster.sync();
+      if (rank == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 3);
 
       // ---- award + apply: the slot holds the highest bid / smallest agent ----
       const int nrec = s_nrec;
@@ -326,6 +331,7 @@ __global__ void __launch_bounds__(kNT, 1) auction_kernel(DevState st, AuctionDev
       if (tid < CS) *cluster.map_shared_rank(&s_cnt[nxt][rank], tid) = s_push;
       if (rank == 0 && tid == 0 && has_deadline && now_ns() >= deadline_gt)
         for (int r = 0; r < CS; ++r) *cluster.map_shared_rank(&s_expired, r) = 1;
+      if (rank == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 4);
       bids += cnt;
       ++round;
       snap = true;
