@@ -120,6 +120,10 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     ch = (ch + 63) / 64 * 64;
     p.chunk = ch;
   }
+  // streaming kernel, single-buffered rows: L2-prefetch the next stage's rows
+  // (LSAPGPU_SCAN_L2PF=0 disables)
+  p.l2_prefetch = p.bufs == 1 ? 1 : 0;
+  if (const char* pf = std::getenv("LSAPGPU_SCAN_L2PF")) p.l2_prefetch = p.bufs == 1 ? std::atoi(pf) : 0;
   p.smem = static_cast<size_t>(p.bufs) * p.m * p.chunk * es + reserve;
   int per_sm = static_cast<int>((227 * 1024) / (p.smem + kStaticSmem + 1024));
   if (per_sm < 1) per_sm = 1;

@@ -267,6 +267,11 @@ __device__ __forceinline__ void compute_step(const StreamRegs<E, M>& r, int32_t 
   }
 }
 
+// L2 prefetch of a byte range (bulk, no completion tracking)
+__device__ __forceinline__ void pf_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // mbarrier arrive (count 1) by one thread
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -279,7 +284,8 @@ constexpr int kMaxBufs = 4;
 
 template <class E, int M, int NT, int KM, bool kChunked, int D>
 __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, int full, int passes,
-                                                          int64_t chunk, int bufs, int max_segments) {
+                                                          int64_t chunk, int bufs, int max_segments,
+                                                          int l2pf) {
   using Acc = typename Traits<E>::Acc;
   constexpr int V = StreamRegs<E, M>::V;
   constexpr int NW = NT / 32;
@@ -381,6 +387,22 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
         for (uint32_t off = 0; off < bytes; off += 32768u) {
           const uint32_t sz = (bytes - off) < 32768u ? (bytes - off) : 32768u;
           bulk_g2s(dst + off, src + off, sz, &full_bar[b]);
+        }
+      }
+      // single-buffered rows: pull the NEXT stage's rows into L2 while this
+      // one is scanned, so its staging copy streams from L2, not HBM
+      if (l2pf && q + 1 < stages) {
+        const int64_t un = blockIdx.x + ((q + 1) / passes) * gridDim.x;
+        const int64_t ln = static_cast<int64_t>((q + 1) % passes) * chunk;
+        const int64_t lenn = (ld - ln) < chunk ? (ld - ln) : chunk;
+        const uint32_t nb = static_cast<uint32_t>(lenn * sizeof(E));
+        const int32_t gn = static_cast<int32_t>(un / S);
+        for (int m = 0; m < M; ++m) {
+          const int32_t idx = gn * M + m;
+          if (idx >= count) break;
+          const int32_t ag = static_cast<int32_t>((full ? static_cast<uint32_t>(idx) : items[idx]) & kItemMask);
+          const unsigned char* src = reinterpret_cast<const unsigned char*>(A + static_cast<int64_t>(ag) * ld + ln);
+          for (uint32_t off = 0; off < nb; off += 32768u) pf_l2(src + off, (nb - off) < 32768u ? (nb - off) : 32768u);
         }
       }
     }
@@ -608,7 +630,7 @@ cudaError_t launch_nt(const DevState& d, const ScanPlan& p, int full, cudaStream
                                        static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;
   return launch_pdl(k, dim3(p.ctas), dim3(NT), p.smem, st, d.pdl, d, full, p.passes, p.chunk, p.bufs,
-                    p.max_segments);
+                    p.max_segments, p.l2_prefetch);
 }
 
 template <class E, int M, int KM>
