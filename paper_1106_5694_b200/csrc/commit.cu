@@ -26,6 +26,7 @@
 #include <cstdlib>
 
 #include "commit_single.cuh"
+#include "commit_apply.cuh"
 #include "state.h"
 
 namespace lsapgpu {
@@ -151,54 +152,11 @@ __global__ void __launch_bounds__(1024, 1)
 // own record was rejected (parallel.cpp:296-330).
 template <class E>
 __global__ void __launch_bounds__(256) commit_apply_kernel(DevState st) {
-  Ctrl* C = st.ctrl;
   pdl_trigger();
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark(C, st.tl, st.tl_cap, 15);
-  const int32_t nlog = C->k2_nlog, nconf = C->k2_nconf;
-  if (nlog + nconf == 0) return;
-  const int32_t n = st.n;
-  const Prop* edges = st.edges[C->k2_parity];
-  const int32_t iter = C->k2_iter;
-  const int64_t base = C->k2_log_base;
-  E* acur = static_cast<E*>(st.acur);
-  int jobs = 0;
-  for (int32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nlog + nconf; x += gridDim.x * blockDim.x) {
-    if (x < nlog) {
-      const Prop p = edges[st.clist[x]];
-      if (p.slot < n) {
-        st.agent_delta[p.a] = 0.0;
-        st.agent_partner[p.a] = -1;
-      } else {
-        st.job_delta[p.j_new] = 0.0;
-        st.job_partner[p.j_new] = -1;
-      }
-      st.sigma[p.j_new] = p.a;
-      st.sigma[p.j_old] = p.d;
-      st.tau[p.a] = p.j_new;
-      st.tau[p.d] = p.j_old;
-      if (st.tau16) {
-        st.tau16[p.a] = static_cast<uint16_t>(p.j_new);
-        st.tau16[p.d] = static_cast<uint16_t>(p.j_old);
-      }
-      acur[p.a] = static_cast<E>(p.acur_a);
-      acur[p.d] = static_cast<E>(p.acur_d);
-      st.log[base + x] = LogEntry{iter, p.slot, p.delta};
-      st.items[2 * x] = static_cast<uint32_t>(p.a) | kItemAgent | kItemJob;
-      st.items[2 * x + 1] = static_cast<uint32_t>(p.d) | kItemAgent | kItemJob;
-    } else {
-      const int32_t q = x - nlog;
-      const Prop p = edges[st.qlist[q]];
-      const int32_t owner = p.slot < n ? p.a : p.d;
-      const int32_t job = p.slot < n ? p.j_old : p.j_new;  // the owner's (unchanged) job
-      const bool jflag = (st.jbits[job >> 5] >> (job & 31)) & 1u;
-      st.items[2 * nlog + q] = static_cast<uint32_t>(owner) | kItemAgent | (jflag ? kItemJob : 0u);
-      jobs += jflag;
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) jobs += __shfl_down_sync(0xffffffffu, jobs, off);
-  if ((threadIdx.x & 31) == 0 && jobs)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&C->job_scans), static_cast<unsigned long long>(jobs));
+  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, 15);
+  apply_batch<E>(st, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                 static_cast<int64_t>(gridDim.x) * blockDim.x);
 }
 
 }  // namespace
@@ -219,6 +177,7 @@ CommitPlan plan_commit(const DevState& d) {
   const size_t budget = 220 * 1024;
   p.cluster_smem = budget;
   p.cluster = commit_cluster_size(d, budget);
+  if (const char* s = std::getenv("LSAPGPU_COMMIT_CS")) p.cluster = std::atoi(s) == 8 ? 8 : p.cluster;
   const size_t kslice = ((static_cast<size_t>(d.n) + p.cluster - 1) / p.cluster * 4 + 15) / 16 * 16;
   const size_t cap = budget > 2 * kslice + 64 ? (budget - 2 * kslice - 64) / 45 : 0;
   p.edge_cap = static_cast<int>(cap / 16 * 16);
@@ -233,6 +192,7 @@ CommitPlan plan_commit(const DevState& d) {
     if (std::atoi(s) == 0) p.cta_edge_cap = 0;
   if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE_MAX")) p.cta_edge_cap = std::min(p.cta_edge_cap, std::atoi(s));
   if (const char* s = std::getenv("LSAPGPU_COMMIT_VARIANT")) p.variant = std::atoi(s);
+  if (const char* s = std::getenv("LSAPGPU_COMMIT_FUSED_APPLY")) p.fused_apply = std::atoi(s) != 0;
   return p;
 }
 
@@ -240,7 +200,7 @@ cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
                           cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st) {
   if (mode == kCommitApplyOnly) return cudaErrorInvalidValue;  // launch_accepted_from_masks
   cudaError_t e = launch_commit_cluster(d, p, mode, cond, use_cond, st);
-  if (e != cudaSuccess || mode != kCommitSolve) return e;
+  if (e != cudaSuccess || mode != kCommitSolve || p.fused_apply) return e;
   return launch_commit_apply(d, st);
 }
 

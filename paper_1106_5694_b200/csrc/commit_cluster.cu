@@ -30,6 +30,7 @@
 
 #include <climits>
 
+#include "commit_apply.cuh"
 #include "commit_single.cuh"
 #include "state.h"
 
@@ -76,7 +77,7 @@ struct EdgeArrays {
 template <class E, int CS>
 __global__ void __launch_bounds__(kNT, 1)
     commit_cluster_kernel(DevState st, int mode, cudaGraphConditionalHandle cond, int use_cond,
-                          int edge_cap, int cta_cap, int var) {
+                          int edge_cap, int cta_cap, int var, int fused) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x;
@@ -128,14 +129,18 @@ __global__ void __launch_bounds__(kNT, 1)
   if (m <= cta_cap && (st.policy == 0 || mode == kCommitCheckOnly)) {
     if (m <= kSingleLoad) {  // few proposals: rank 0 loads them itself
       if (rank == 0) single::commit_single(st, mode, cta_cap, smem);
-      return;
+    } else {  // many: every rank loads a share straight into rank 0's shared memory
+      unsigned char* dst = cluster.map_shared_rank(smem, 0);
+      const int32_t per = (m + CS - 1) / CS;
+      single::load_share(st, cta_cap, dst, min(m, rank * per), min(m, (rank + 1) * per));
+      cluster.sync();
+      if (rank == 0) single::commit_single(st, mode, cta_cap, smem, true);
     }
-    // many: every rank loads a share straight into rank 0's shared memory
-    unsigned char* dst = cluster.map_shared_rank(smem, 0);
-    const int32_t per = (m + CS - 1) / CS;
-    single::load_share(st, cta_cap, dst, min(m, rank * per), min(m, (rank + 1) * per));
-    cluster.sync();
-    if (rank == 0) single::commit_single(st, mode, cta_cap, smem, true);
+    if (mode == kCommitSolve && fused) {  // the batch's scattered writes, cluster-wide
+      cluster.sync();
+      if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 15);
+      apply_batch<E>(st, static_cast<int64_t>(rank) * kNT + tid, static_cast<int64_t>(CS) * kNT);
+    }
     return;
   }
   const int32_t iter = C->iter + 1;
@@ -342,6 +347,11 @@ __global__ void __launch_bounds__(kNT, 1)
       if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
       tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
     }
+    if (mode == kCommitSolve && fused) {
+      cluster.sync();  // batch counters written
+      if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 15);
+      apply_batch<E>(st, static_cast<int64_t>(rank) * kNT + tid, static_cast<int64_t>(CS) * kNT);
+    }
     return;
   }
 
@@ -501,7 +511,8 @@ cudaError_t launch_cs(const DevState& d, const CommitPlan& p, int mode, cudaGrap
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = d.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap, p.variant);
+  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap, p.variant,
+                            p.fused_apply);
 }
 
 template <int CS>

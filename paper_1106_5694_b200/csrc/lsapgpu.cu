@@ -1191,7 +1191,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       if (multi) {
         for (;;) {
           CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
-          ctx->launches += 2;  // conflict check + apply
+          ctx->launches += ctx->commit_plan.launches();  // conflict check (+ apply)
           rc = pull_ctrl(ctx);
           if (rc) return rc;
           const Ctrl& C = *ctx->ctrl_host;
@@ -1221,7 +1221,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
             ctx->commit_ms += cms;
             ++ctx->commit_launches;
           }
-          ctx->launches += 2;  // conflict check + apply
+          ctx->launches += ctx->commit_plan.launches();  // conflict check (+ apply)
           rc = run_scan(ctx, 0);
           if (rc) return rc;
           ++launches;
@@ -1294,7 +1294,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   // every body pass of the graph is a commit (conflict check + apply) and a
   // scan launch; the last pass per graph launch finds no active record and
   // exits early
-  if (graphed) ctx->launches += 3 * (S.inner_iterations + graph_launches);
+  if (graphed) ctx->launches += (1 + ctx->commit_plan.launches()) * (S.inner_iterations + graph_launches);
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 

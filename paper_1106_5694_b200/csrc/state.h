@@ -147,11 +147,15 @@ struct CommitPlan {
   size_t cluster_smem = 0;  // cluster kernel: dynamic smem per CTA
   int edge_cap = 0;         // cluster kernel: proposals per CTA held in smem
   int cta_edge_cap = 0;     // single-CTA path taken when the proposals fit one CTA (0: never)
-  int variant = 1;          // cluster kernel bit 0: read keys before the round-1 atomics
+  int variant = 0;          // cluster kernel bit 0: read keys before the round-1 atomics
+  int fused_apply = 0;      // split commit: the cluster kernel runs the apply itself (1, opt-in:
+                            // measured 7 % slower at C3, 16 SMs of one GPC issue the scattered
+                            // writes) or commit_apply_kernel follows it on 64 SMs (0)
+  int launches() const { return fused_apply ? 1 : 2; }  // kernels per solve-mode commit
   bool operator==(const CommitPlan& o) const {
     return threads == o.threads && smem == o.smem && keys_in_smem == o.keys_in_smem && cluster == o.cluster &&
            cluster_smem == o.cluster_smem && edge_cap == o.edge_cap && cta_edge_cap == o.cta_edge_cap &&
-           variant == o.variant;
+           variant == o.variant && fused_apply == o.fused_apply;
   }
 };
 CommitPlan plan_commit(const DevState& d);

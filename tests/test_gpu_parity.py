@@ -113,6 +113,8 @@ def test_generators_match_oracle(oracle, gpu_ctx):
 @pytest.mark.parametrize("env", [
     {},                                                                # resident-state kernel (default)
     {"LSAPGPU_COMMIT_SINGLE": "0"},                                    # cluster commit for every batch
+    {"LSAPGPU_COMMIT_FUSED_APPLY": "1"},                               # apply inside the cluster kernel
+    {"LSAPGPU_COMMIT_FUSED_APPLY": "1", "LSAPGPU_COMMIT_SINGLE": "0"},
     {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
     {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
