@@ -132,3 +132,28 @@ def test_auction_constant_matrix_uses_unit_epsilon(oracle, gpu_ctx):
     assert rep.gpu["epsilon"] == 1.0
     assert (rep.assignment.sigma == want.sigma).all()
     assert rep.outer_iterations == want.rounds
+
+
+@pytest.mark.parametrize("name", ["c1_int1000", "geom128_s31", "p2p1000_scaling_sf2"])
+def test_auction_global_prices_path(oracle, gpu_ctx, name, monkeypatch):
+    """Prices read from global memory (the n > 20480 configuration) on small cases."""
+    monkeypatch.setenv("LSAPGPU_AUCTION_LOCAL_PRICES", "0")
+    rec = GOLD[name]
+    load(gpu_ctx, oracle, rec)
+    rep = gpu_ctx.auction_solve(acfg(rec))
+    assert sha(rep.assignment.sigma) == rec["sigma_sha"]
+    assert float(rep.assignment.value).hex() == rec["value_hex"]
+    assert rep.outer_iterations == rec["rounds"]
+    assert sha(rep.gpu["prices"]) == rec["prices_sha"]
+
+
+def test_auction_large_n_global_prices(oracle, gpu_ctx):
+    """n above the shared-memory price replica: global-price bidding, vs the oracle."""
+    import paper_1106_5694_b200 as g
+    n = 21000
+    gpu_ctx.generate("int", n, 5, 1000.0)
+    rep = gpu_ctx.auction_solve(g.AuctionConfig(epsilon=4.0))
+    a = oracle.generate("int", n, 5, 1000.0)
+    want = oracle.auction_solve(a, epsilon=4.0)
+    assert (rep.assignment.sigma == want.sigma).all()
+    assert rep.outer_iterations == want.rounds and rep.switches_applied == want.switches
