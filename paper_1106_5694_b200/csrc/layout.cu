@@ -82,22 +82,29 @@ __global__ void gen_aux_kernel(LayoutSource s, int32_t n, double* aux) {
   }
 }
 
+// Storage flags of one entry (bit0 non-finite, bit1 not int16-exact, bit2 not
+// an integer below 2^29, bit3 not fp32-exact), with two conversions for the
+// common integer case: one saturating double->int and back decides
+// integrality and both integer ranges; values that are int16-exact are
+// fp32-exact, so the float round trip runs only for the others.
+__device__ __forceinline__ uint32_t entry_flags(double v) {
+  if (!isfinite(v)) return 1u | 2u | 4u | 8u;
+  const int32_t iv = __double2int_rz(v);  // saturates
+  const bool integral = static_cast<double>(iv) == v;
+  const uint32_t a = static_cast<uint32_t>(iv < 0 ? -static_cast<int64_t>(iv) : iv);
+  if (integral && a <= 32767u) return 0u;
+  uint32_t f = 2u;
+  if (!(integral && a < 536870912u)) f |= 4u;
+  if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
+  return f;
+}
+
 __global__ void classify_kernel(Src src, int64_t row0, int64_t rows, uint32_t* flags) {
   uint32_t f = 0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-    const int64_t i = row0 + r;
-    for (int32_t j = threadIdx.x; j < src.n; j += blockDim.x) {
-      const double v = src(i, j);
-      if (!isfinite(v)) {
-        f |= 1u | 2u | 4u | 8u;
-        continue;
-      }
-      const bool integral = v == trunc(v);
-      if (!(integral && fabs(v) <= 32767.0)) f |= 2u;
-      if (!(integral && fabs(v) < 536870912.0)) f |= 4u;
-      if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
-    }
-  }
+  const int64_t total = rows * src.n;  // flat over the block of rows: every thread busy
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    f |= entry_flags(src(row0 + e / src.n, static_cast<int32_t>(e % src.n)));
   // warp then block OR, one atomic per block
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
   __shared__ uint32_t wf[32];
@@ -112,10 +119,12 @@ __global__ void classify_kernel(Src src, int64_t row0, int64_t rows, uint32_t* f
 
 template <class E>
 __device__ __forceinline__ E narrow(double v) {
+  // (truncating conversion: the stored values are exact integers, and it is
+  // the same instruction entry_flags issues)
   if constexpr (sizeof(E) == 2)
-    return static_cast<int16_t>(__double2int_rn(v));
+    return static_cast<int16_t>(__double2int_rz(v));
   else if constexpr (Traits<E>::kInt)
-    return static_cast<int32_t>(__double2int_rn(v));
+    return static_cast<int32_t>(__double2int_rz(v));
   else if constexpr (sizeof(E) == 4)
     return __double2float_rn(v);
   else
@@ -151,6 +160,29 @@ __global__ void build_layout_kernel(Src src, int64_t row0, int64_t rows, E* A, E
 // the flags demand a wider type).  64x64 tiles, 256 threads: each lane owns
 // two adjacent columns, so the source reads, the A-row writes and the AT-row
 // writes are all coalesced.
+// Two adjacent elements in one store (the pair is 2-element aligned: ld is a
+// multiple of 64 and the column even).
+template <class E>
+struct Pair;
+template <>
+struct Pair<int16_t> {
+  __device__ static void st(int16_t* p, int16_t a, int16_t b) {
+    *reinterpret_cast<uint32_t*>(p) = static_cast<uint16_t>(a) | (static_cast<uint32_t>(static_cast<uint16_t>(b)) << 16);
+  }
+};
+template <>
+struct Pair<int32_t> {
+  __device__ static void st(int32_t* p, int32_t a, int32_t b) { *reinterpret_cast<int2*>(p) = make_int2(a, b); }
+};
+template <>
+struct Pair<float> {
+  __device__ static void st(float* p, float a, float b) { *reinterpret_cast<float2*>(p) = make_float2(a, b); }
+};
+template <>
+struct Pair<double> {
+  __device__ static void st(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
+};
+
 template <class E>
 __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0, int64_t rows, E* A, E* AT,
                                                            int64_t ld, uint32_t* flags) {
@@ -162,46 +194,36 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
   const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;  // 8 row groups
   const int64_t j = bj + 2 * lane;
   uint32_t f = 0;
-  for (int r = rg; r < 64; r += 8) {
+  // all eight rows' loads first (8 x 16 B in flight per lane), then classify / store
+  double v[8][2];
+  const bool fast = src.s.kind == 0 && src.s.src_dtype == 0 && j + 1 < n && (n & 1) == 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t i = bi + rg + 8 * q;
+    v[q][0] = v[q][1] = 0.0;
+    if (i >= rend) continue;
+    if (fast) {  // fp64 memory source, even n: both columns in one aligned 16-byte load
+      const double2 w = __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(src.s.src) + i * n + j));
+      v[q][0] = w.x;
+      v[q][1] = w.y;
+    } else {
+      if (j < n) v[q][0] = src(i, j);
+      if (j + 1 < n) v[q][1] = src(i, j + 1);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = rg + 8 * q;
     const int64_t i = bi + r;
     if (i >= rend) break;
-    double v0 = 0.0, v1 = 0.0;
-    if (src.s.kind == 0 && src.s.src_dtype == 0 && j + 1 < n) {
-      // fp64 memory source: both columns in one 16-byte load when aligned
-      const double* p = static_cast<const double*>(src.s.src) + i * n + j;
-      if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-        const double2 w = __ldg(reinterpret_cast<const double2*>(p));
-        v0 = w.x;
-        v1 = w.y;
-      } else {
-        v0 = p[0];
-        v1 = p[1];
-      }
-    } else {
-      if (j < n) v0 = src(i, j);
-      if (j + 1 < n) v1 = src(i, j + 1);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const double v = h ? v1 : v0;
-      if (j + h >= n) continue;
-      if (!isfinite(v)) {
-        f |= 1u | 2u | 4u | 8u;
-      } else {
-        const bool integral = v == trunc(v);
-        if (!(integral && fabs(v) <= 32767.0)) f |= 2u;
-        if (!(integral && fabs(v) < 536870912.0)) f |= 4u;
-        if (static_cast<double>(__double2float_rn(v)) != v) f |= 8u;
-      }
-    }
+    const double v0 = v[q][0], v1 = v[q][1];
+    if (j < n) f |= entry_flags(v0);
+    if (j + 1 < n) f |= entry_flags(v1);
     const E e0 = narrow<E>(isfinite(v0) ? v0 : 0.0), e1 = narrow<E>(isfinite(v1) ? v1 : 0.0);
-    if (j + 1 < n) {
-      E* a = A + i * ld + j;
-      a[0] = e0;
-      a[1] = e1;
-    } else if (j < n) {
+    if (j + 1 < n)
+      Pair<E>::st(A + i * ld + j, e0, e1);
+    else if (j < n)
       A[i * ld + j] = e0;
-    }
     tile[r][2 * lane] = e0;
     tile[r][2 * lane + 1] = e1;
   }
@@ -212,12 +234,10 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
     const int64_t jj = bj + c;
     if (jj >= n) break;
     E* at = AT + jj * ld + ia;
-    if (ia + 1 < rend) {
+    if (ia + 1 < rend)
+      Pair<E>::st(at, tile[2 * lane][c], tile[2 * lane + 1][c]);
+    else if (ia < rend)
       at[0] = tile[2 * lane][c];
-      at[1] = tile[2 * lane + 1][c];
-    } else if (ia < rend) {
-      at[0] = tile[2 * lane][c];
-    }
   }
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
   __shared__ uint32_t wf[8];
