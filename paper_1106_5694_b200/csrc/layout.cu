@@ -262,11 +262,17 @@ __global__ void init_assignment_kernel(DevState d) {
 }
 
 template <class E>
-__global__ void gather_current_kernel(DevState d, double* out) {
+__global__ void gather_current_kernel(DevState d, double* out, int pack) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.n) return;
   const E* A = static_cast<const E*>(d.A);
-  out[j] = static_cast<double>(A[static_cast<int64_t>(d.sigma[j]) * d.ld + j]);
+  const int32_t sj = d.sigma[j];
+  out[j] = static_cast<double>(A[static_cast<int64_t>(sj) * d.ld + j]);
+  if (pack) {  // [values | sigma | tau] for one device->host copy
+    int32_t* w = reinterpret_cast<int32_t*>(out + d.n);
+    w[j] = sj;
+    w[d.n + j] = d.tau[j];
+  }
 }
 
 template <class E>
@@ -313,8 +319,8 @@ struct InitK {
 };
 template <class E>
 struct GatherK {
-  static void run(dim3 g, dim3 b, cudaStream_t st, DevState d, double* out) {
-    gather_current_kernel<E><<<g, b, 0, st>>>(d, out);
+  static void run(dim3 g, dim3 b, cudaStream_t st, DevState d, double* out, int pack) {
+    gather_current_kernel<E><<<g, b, 0, st>>>(d, out, pack);
   }
 };
 template <class E>
@@ -361,8 +367,8 @@ cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st) {
   return dispatch<InitK>(d.storage, dim3((d.n + 255) / 256), dim3(256), st, d);
 }
 
-cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st) {
-  return dispatch<GatherK>(d.storage, dim3((d.n + 255) / 256), dim3(256), st, d, out);
+cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st, int pack) {
+  return dispatch<GatherK>(d.storage, dim3((d.n + 255) / 256), dim3(256), st, d, out, pack);
 }
 
 cudaError_t launch_read_rows(const DevState& d, const int32_t* rows, int32_t nrows, double* out,

@@ -11,6 +11,7 @@
 // termination test (parallel.cpp:306-310, 343-345).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <condition_variable>
 #include <cstdlib>
@@ -193,6 +194,12 @@ struct lsapgpu_ctx {
 
   // auction baseline (auction.cu): per-n vectors (in vec_bufs), the epsilon
   // schedule and the benefit range of the current matrix
+  // cached random_perm(n, seed) and the counter base of a solve (pinned)
+  int32_t* perm_pin = nullptr;
+  int32_t perm_cap = 0, perm_n = -1;
+  uint64_t perm_seed = 0;
+  Ctrl* ctrl_base = nullptr;
+
   AuctionDev au;
   int32_t au_n = 0;
   AuctionCtrl* au_host = nullptr;  // pinned
@@ -529,19 +536,19 @@ bool is_perm(const int32_t* p, int32_t n) {
 // Ordered objective (core.cpp:17-24) over the device matrix and a device sigma.
 // Enqueue the objective gather into pinned memory (no sync); objective_sum
 // adds it up in job order once the stream has been synchronised.
-int enqueue_objective(lsapgpu_ctx* ctx) {
+int enqueue_objective(lsapgpu_ctx* ctx, bool pack = false) {
   const int32_t n = ctx->d.n;
   if (ctx->obj_cap < n) {
     if (ctx->obj_pin) cudaFreeHost(ctx->obj_pin);
     ctx->obj_pin = nullptr;
     ctx->obj_cap = 0;
-    CK(cudaMallocHost(&ctx->obj_pin, sizeof(double) * n));
+    CK(cudaMallocHost(&ctx->obj_pin, sizeof(double) * 2 * n));  // room for the packed sigma / tau
     ctx->obj_cap = n;
   }
   double* dv = reinterpret_cast<double*>(ctx->d.c_delta);  // scratch (2n doubles)
-  CK(launch_gather_current(ctx->d, dv, ctx->stream));
+  CK(launch_gather_current(ctx->d, dv, ctx->stream, pack ? 1 : 0));
   ++ctx->launches;
-  CK(cpy(ctx, ctx->obj_pin, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, ctx->obj_pin, dv, sizeof(double) * (pack ? 2 : 1) * n, cudaMemcpyDeviceToHost, ctx->stream));
   return LSAPGPU_OK;
 }
 double objective_sum(const lsapgpu_ctx* ctx) {  // core.cpp:17-24: ordered sum over jobs
@@ -717,6 +724,8 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   if (ctx->d.tl) cudaFree(ctx->d.tl);
   if (ctx->obj_pin) cudaFreeHost(ctx->obj_pin);
   if (ctx->au_host) cudaFreeHost(ctx->au_host);
+  if (ctx->perm_pin) cudaFreeHost(ctx->perm_pin);
+  if (ctx->ctrl_base) cudaFreeHost(ctx->ctrl_base);
   if (ctx->eps_dev) cudaFree(ctx->eps_dev);
   if (ctx->log_pin) cudaFreeHost(ctx->log_pin);
   if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
@@ -1118,26 +1127,49 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     return LSAPGPU_OK;
   };
 
-  std::vector<int32_t> sigma0(n);
+  // initial permutation: random_perm(seed) is sequential by nature and a pure
+  // function of (n, seed), so the last one is kept in pinned memory
   if (P.init_sigma) {
     if (!is_perm(P.init_sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
-    std::copy(P.init_sigma, P.init_sigma + n, sigma0.begin());
+    CK(cpy(ctx, d.sigma, P.init_sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   } else {
-    lsapgpu_random_perm(n, P.seed, sigma0.data());
+    if (ctx->perm_n != n || ctx->perm_seed != P.seed) {
+      CK(cudaStreamSynchronize(ctx->stream));  // a previous upload may still read the buffer
+      if (ctx->perm_cap < n) {
+        if (ctx->perm_pin) cudaFreeHost(ctx->perm_pin);
+        ctx->perm_pin = nullptr;
+        ctx->perm_cap = 0;
+        CK(cudaMallocHost(&ctx->perm_pin, sizeof(int32_t) * n));
+        ctx->perm_cap = n;
+      }
+      lsapgpu_random_perm(n, P.seed, ctx->perm_pin);
+      ctx->perm_n = n;
+      ctx->perm_seed = P.seed;
+    }
+    CK(cpy(ctx, d.sigma, ctx->perm_pin, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   }
-  CK(cpy(ctx, d.sigma, sigma0.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(launch_init_assignment(d, ctx->stream));
   ++ctx->launches;
-  // initial objective and the counter base, read back with ONE sync
+  // initial objective and the counter base: enqueued now, read at the first
+  // sync the solve needs anyway (the device starts the first sweep at once)
   int rc = enqueue_objective(ctx);
   if (rc) return rc;
-  CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  double value = objective_sum(ctx);
-  const Ctrl base = *ctx->ctrl_host;  // counters are cumulative per context
-
+  if (!ctx->ctrl_base) CK(cudaMallocHost(&ctx->ctrl_base, sizeof(Ctrl)));
+  CK(cpy(ctx, ctx->ctrl_base, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  double value = 0.0;
+  Ctrl base;
+  std::memset(&base, 0, sizeof(base));
+  bool inited = false;
   TraceSink trace{trace_switch, trace_value, trace_cap};
-  trace.push(0, value);
+  auto ensure_init = [&]() -> int {
+    if (inited) return LSAPGPU_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    value = objective_sum(ctx);
+    base = *ctx->ctrl_base;  // counters are cumulative per context
+    trace.push(0, value);
+    inited = true;
+    return LSAPGPU_OK;
+  };
   lsapgpu_stats S;
   std::memset(&S, 0, sizeof(S));
   S.storage = d.storage;
@@ -1146,6 +1178,13 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_start)
         .count();
   };
+  // LSAPGPU_HOST_TIMING=1: host-side phase marks of this solve on stderr
+  static const bool host_timing = std::getenv("LSAPGPU_HOST_TIMING") != nullptr;
+  std::vector<std::pair<const char*, int64_t>> hmarks;
+  auto hmark = [&](const char* what) {
+    if (host_timing) hmarks.emplace_back(what, elapsed_ns());
+  };
+  hmark("init+objective");
   bool expired = P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns;
 
   d.eps = P.eps;
@@ -1173,7 +1212,8 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
 
   while (!expired) {
     ++S.outer_iterations;
-    const double f_start = value;
+    double f_start = value;  // (first pass: set once the initial objective is read)
+    const bool first_pass = !inited;
     begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
     ++ctx->launches;
     CK(cudaGetLastError());
@@ -1207,7 +1247,9 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cpy(ctx, ctx->log_pin, d.log, sizeof(LogEntry) * std::min<int64_t>(lsapgpu_ctx::kLogPin, d.log_cap),
                cudaMemcpyDeviceToHost, ctx->stream));
+        hmark("graph launched");
         CK(cudaStreamSynchronize(ctx->stream));
+        hmark("graph done");
         prefetched = true;
       } else {
         for (;;) {
@@ -1231,6 +1273,8 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
           if (C.inner_done || C.expired || C.drain || C.error) break;
         }
       }
+      if ((rc = ensure_init())) return rc;
+      if (first_pass) f_start = value;
       Ctrl& C = *ctx->ctrl_host;
       if (C.error) {
         C.error = 0;
@@ -1238,26 +1282,43 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
       }
       const int64_t cnt = C.log_count;
-      log.resize(static_cast<size_t>(cnt));
       const int64_t have = prefetched ? std::min<int64_t>(cnt, lsapgpu_ctx::kLogPin) : 0;
-      if (have) std::memcpy(log.data(), ctx->log_pin, sizeof(LogEntry) * have);
-      if (cnt > have) {
-        CK(cpy(ctx, log.data() + have, d.log + have, sizeof(LogEntry) * (cnt - have), cudaMemcpyDeviceToHost,
-               ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-      }
-      prefetched = false;
       // Replay in the reference's batch order (iteration, then ascending slot:
       // agents then jobs, parallel.cpp:306-310).  Integer deltas sum exactly in
       // any order, so without a trace the order only matters for float storage.
       const bool need_order = (trace_switch && trace_value) || d.storage == kF32 || d.storage == kF64;
-      if (need_order) order_log(log, sorted, 2 * n);
-      const std::vector<LogEntry>& seq = need_order ? sorted : log;
-      for (const auto& L : seq) {
-        value += L.delta;
-        ++switches;
-        trace.push(switches, value);
+      const LogEntry* entries = ctx->log_pin;
+      if (need_order || cnt > have) {
+        log.resize(static_cast<size_t>(cnt));
+        if (have) std::memcpy(log.data(), ctx->log_pin, sizeof(LogEntry) * have);
+        if (cnt > have) {
+          CK(cpy(ctx, log.data() + have, d.log + have, sizeof(LogEntry) * (cnt - have), cudaMemcpyDeviceToHost,
+                 ctx->stream));
+          CK(cudaStreamSynchronize(ctx->stream));
+        }
+        entries = log.data();
       }
+      prefetched = false;
+      if (need_order) {
+        order_log(log, sorted, 2 * n);
+        for (const auto& L : sorted) {
+          value += L.delta;
+          ++switches;
+          trace.push(switches, value);
+        }
+      } else {
+        // integer storage, no trace: every delta and partial sum is an exact
+        // integer, so independent partial sums give the sequential result
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int64_t k = 0;
+        for (; k + 4 <= cnt; k += 4)
+          for (int q = 0; q < 4; ++q) acc[q] += entries[k + q].delta;
+        for (; k < cnt; ++k) acc[0] += entries[k].delta;
+        value += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        switches += cnt;
+        trace.len = std::min<int64_t>(kTraceCap, trace.len + cnt);  // what push() would count
+      }
+      hmark("log replayed");
       const bool drained = C.drain;
       if (C.expired) expired = true;
       begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);
@@ -1274,14 +1335,25 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     if (value == f_start) break;
   }
 
+  if ((rc = ensure_init())) return rc;  // (a solve cut before its first pass)
   // final counters, sigma / tau and the ordered objective with ONE sync
   CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cpy(ctx, sigma_out, d.sigma, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (tau_out) CK(cpy(ctx, tau_out, d.tau, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  rc = enqueue_objective(ctx);  // snapshot_assignment, solver_state.hpp:141-148
+  rc = enqueue_objective(ctx, true);  // snapshot_assignment (solver_state.hpp:141-148) + sigma / tau
   if (rc) return rc;
+  hmark("final enqueued");
   CK(cudaStreamSynchronize(ctx->stream));
   const double final_value = objective_sum(ctx);
+  {
+    const int32_t* packed = reinterpret_cast<const int32_t*>(ctx->obj_pin + n);
+    std::memcpy(sigma_out, packed, sizeof(int32_t) * n);
+    if (tau_out) std::memcpy(tau_out, packed + n, sizeof(int32_t) * n);
+  }
+  hmark("final done");
+  if (host_timing) {
+    std::string line = "lsapgpu host timing (us):";
+    for (const auto& m : hmarks) line += std::string(" ") + m.first + "=" + std::to_string(m.second / 1000);
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
   const Ctrl& C = *ctx->ctrl_host;
   S.inner_iterations = C.inner_iterations - base.inner_iterations;
   S.pair_items += C.pair_items - base.pair_items;

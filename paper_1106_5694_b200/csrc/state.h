@@ -101,7 +101,8 @@ cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaSt
 cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
                                 void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st);
 cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st);  // tau, acur from sigma
-cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st);
+// out[j] = A[sigma[j]][j] (fp64); pack: also sigma and tau as int32 after it (2n doubles)
+cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st, int pack = 0);
 cudaError_t launch_read_rows(const DevState& d, const int32_t* rows, int32_t nrows, double* out,
                              cudaStream_t st);
 
