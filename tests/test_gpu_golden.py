@@ -91,3 +91,20 @@ def test_step_apis_vs_reference(oracle, gpu_ctx, key):
     assert float(out.value).hex() == rec["value_after_hex"]
     assert [[x.agent, x.new_job, x.old_job, x.displaced] for x in applied] == ARR[f"{key}__applied"].tolist()
     assert [x.delta for x in applied] == ARR[f"{key}__applied_delta"].tolist()
+
+
+@pytest.mark.parametrize("name", ["c1_int1000", "c2_int5000", "c3_p2p10000", "int10000", "f32_10000",
+                                  "c2_int5000_touched_only", "geom2048"])
+@pytest.mark.parametrize("graph", [True, False])
+def test_config_solves_without_trace(gpu_ctx, name, graph):
+    """The bench path (no trace buffers): integer storage replays the delta
+    log as exact partial sums; results must still equal the reference's."""
+    rec = GOLD["solves"][name]
+    gpu_ctx.generate(rec["kind"], rec["n"], rec["instance_seed"], rec["param"])
+    rep = gpu_ctx.solve(cfg(rec, use_graph=graph), trace=False)
+    assert sha(rep.assignment.sigma) == rec["sigma_sha"]
+    assert sha(rep.assignment.tau) == rec["tau_sha"]
+    assert float(rep.assignment.value).hex() == rec["value_hex"]
+    assert rep.outer_iterations == rec["outer"]
+    assert rep.switches_applied == rec["switches"]
+    assert rep.gpu["trace_len"] == rec["trace_len"]
