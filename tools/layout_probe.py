@@ -1,5 +1,5 @@
 """Time set_matrix from a device-resident fp64 matrix (the bench 'value' layout phase)."""
-import os, sys, time
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1106_5694_b200 as g

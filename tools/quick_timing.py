@@ -1,4 +1,4 @@
-import sys, time, numpy as np
+import sys, time
 sys.path.insert(0, '.')
 import paper_1106_5694_b200 as g
 from oracle.oracle import Oracle

@@ -1,5 +1,5 @@
 """Sweep scan plans (M items per CTA stage, B staged buffers) in fresh processes."""
-import itertools, json, os, subprocess, sys
+import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 code = r'''
 import sys, json; sys.path.insert(0, %r)
