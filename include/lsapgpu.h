@@ -75,8 +75,14 @@ typedef struct {
   int32_t reeval;             /* LSAPGPU_REEVAL_* */
   int32_t use_graph;          /* 1: inner loop as one CUDA-graph launch (default); 0: host-stepped */
   int64_t deadline_ns;        /* DgsConfig::deadline; < 0 = none */
-  const int32_t* init_sigma;  /* optional initial sigma (job -> agent); NULL = random_perm(seed) */
+  const int32_t* init_sigma;  /* optional initial sigma (job -> agent); NULL = init_mode below */
+  int32_t init_mode;          /* without init_sigma: LSAPGPU_INIT_RANDOM = random_perm(seed), the
+                                 reference's initial_random (dgs.cpp:22-25); LSAPGPU_INIT_GREEDY =
+                                 the device greedy assignment (extension, lsapgpu_greedy_assignment) */
+  int32_t pad_;
 } lsapgpu_params;
+#define LSAPGPU_INIT_RANDOM 0
+#define LSAPGPU_INIT_GREEDY 1
 
 typedef struct {
   int64_t outer_iterations;   /* SolveReport::outer_iterations */
@@ -212,6 +218,13 @@ typedef struct {
 int lsapgpu_auction_solve(lsapgpu_ctx* ctx, const lsapgpu_auction_params* params, int32_t* sigma_out,
                           int32_t* tau_out, lsapgpu_auction_stats* stats, double* prices_out,
                           double* round_prices, int64_t round_cap);
+
+/* Greedy assignment of the context's matrix (EXTENSION, not in the
+ * reference: north-star item 2).  Rounds of: every unassigned agent claims its
+ * best free job (row argmax, smallest job on ties); each claimed job goes to
+ * the highest claim (smallest agent on ties); losers retry.  sigma_out: job ->
+ * agent (n); *rounds (nullable) the number of claim rounds. */
+int lsapgpu_greedy_assignment(lsapgpu_ctx* ctx, int32_t* sigma_out, int64_t* rounds);
 
 /* Host helpers (sequential by nature; identical to the reference's). */
 void lsapgpu_random_perm(int32_t n, uint64_t seed, int32_t* out);

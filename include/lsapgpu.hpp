@@ -37,7 +37,8 @@ namespace lsap::gpu {
 
 struct GpuConfig : ParallelConfig {
   int device = 0;
-  bool use_graph = true;  // inner loop as one CUDA-graph launch per outer pass
+  bool use_graph = true;     // inner loop as one CUDA-graph launch per outer pass
+  bool greedy_init = false;  // extension: start from the device greedy assignment, not initial_random
 };
 
 class Context {
@@ -92,6 +93,7 @@ inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {})
   p.use_graph = cfg.use_graph ? 1 : 0;
   p.deadline_ns = cfg.deadline ? static_cast<std::int64_t>(cfg.deadline->count()) : -1;
   p.init_sigma = nullptr;
+  p.init_mode = cfg.greedy_init ? LSAPGPU_INIT_GREEDY : LSAPGPU_INIT_RANDOM;
   const std::int32_t n = inst.n;
   SolveReport rep;
   rep.assignment.sigma.resize(n);

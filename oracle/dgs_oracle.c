@@ -483,10 +483,81 @@ static void push_trace(int64_t* ts, double* tv, int64_t cap, int64_t* len, int64
 }
 
 /* parallel.cpp:231-352 */
+static int dgs_run(const double* a, int32_t n, uint64_t seed, const int32_t* init_sigma, double eps,
+                   int policy, int64_t deadline_ns, int threads, int32_t* sigma_out, int32_t* tau_out,
+                   orc_stats* stats, int64_t* trace_switch, double* trace_value, int64_t trace_cap,
+                   int64_t* trace_len);
+
 int orc_dgs_parallel(const double* a, int32_t n, uint64_t seed, double eps, int policy,
                      int64_t deadline_ns, int threads, int32_t* sigma_out, int32_t* tau_out,
                      orc_stats* stats, int64_t* trace_switch, double* trace_value,
                      int64_t trace_cap, int64_t* trace_len) {
+  return dgs_run(a, n, seed, NULL, eps, policy, deadline_ns, threads, sigma_out, tau_out, stats, trace_switch,
+                 trace_value, trace_cap, trace_len);
+}
+
+int orc_dgs_parallel_from(const double* a, int32_t n, const int32_t* init_sigma, double eps, int policy,
+                          int64_t deadline_ns, int threads, int32_t* sigma_out, int32_t* tau_out,
+                          orc_stats* stats, int64_t* trace_switch, double* trace_value,
+                          int64_t trace_cap, int64_t* trace_len) {
+  return dgs_run(a, n, 0, init_sigma, eps, policy, deadline_ns, threads, sigma_out, tau_out, stats, trace_switch,
+                 trace_value, trace_cap, trace_len);
+}
+
+int64_t orc_greedy_assignment(const double* a, int32_t n, int32_t* sigma_out) {
+  const size_t N = (size_t)n;
+  uint8_t* taken = (uint8_t*)calloc(N, 1);
+  int32_t* un = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* claim = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* winner = (int32_t*)malloc(sizeof(int32_t) * N);
+  double* wval = (double*)malloc(sizeof(double) * N);
+  int32_t cnt = n;
+  int64_t rounds = 0;
+  for (int32_t i = 0; i < n; ++i) un[i] = i;
+  for (int32_t j = 0; j < n; ++j) winner[j] = -1;
+  while (cnt > 0) {
+    ++rounds;
+    for (int32_t k = 0; k < cnt; ++k) {  /* ascending agents within the list order */
+      const int32_t i = un[k];
+      const double* row = a + (size_t)i * N;
+      int32_t bj = -1;
+      double bv = -INFINITY;
+      for (int32_t j = 0; j < n; ++j)
+        if (!taken[j] && (bj < 0 || row[j] > bv)) {
+          bv = row[j];
+          bj = j;
+        }
+      claim[i] = bj;
+      if (winner[bj] < 0 || bv > wval[bj] || (bv == wval[bj] && i < winner[bj])) {
+        winner[bj] = i;
+        wval[bj] = bv;
+      }
+    }
+    int32_t m = 0;
+    for (int32_t k = 0; k < cnt; ++k) {
+      const int32_t i = un[k], j = claim[i];
+      if (winner[j] == i) {
+        sigma_out[j] = i;
+        taken[j] = 1;
+      } else {
+        un[m++] = i;
+      }
+    }
+    for (int32_t j = 0; j < n; ++j) winner[j] = -1;
+    cnt = m;
+  }
+  free(taken);
+  free(un);
+  free(claim);
+  free(winner);
+  free(wval);
+  return rounds;
+}
+
+static int dgs_run(const double* a, int32_t n, uint64_t seed, const int32_t* init_sigma, double eps,
+                   int policy, int64_t deadline_ns, int threads, int32_t* sigma_out, int32_t* tau_out,
+                   orc_stats* stats, int64_t* trace_switch, double* trace_value, int64_t trace_cap,
+                   int64_t* trace_len) {
   int rc = orc_validate(a, n);
   if (rc) return rc;
   if (!(eps >= 0.0)) return 2;
@@ -500,7 +571,10 @@ int orc_dgs_parallel(const double* a, int32_t n, uint64_t seed, double eps, int 
 
   /* initial_random: dgs.cpp:22-25 */
   int32_t* perm = (int32_t*)malloc(sizeof(int32_t) * N);
-  orc_random_perm(n, seed, perm);
+  if (init_sigma)
+    memcpy(perm, init_sigma, sizeof(int32_t) * N);
+  else
+    orc_random_perm(n, seed, perm);
   state_t st;
   if (state_init(&st, a, n, perm) != 0) {
     free(perm);

@@ -109,6 +109,20 @@ int orc_dgs_parallel(const double* a, int32_t n, uint64_t seed, double eps, int 
                      orc_stats* stats, int64_t* trace_switch, double* trace_value,
                      int64_t trace_cap, int64_t* trace_len);
 
+/* The same loop from a caller-given initial sigma (job -> agent) instead of
+ * initial_random: the parity checker of the device's greedy-start solves (an
+ * extension; the reference itself always starts from initial_random). */
+int orc_dgs_parallel_from(const double* a, int32_t n, const int32_t* init_sigma, double eps, int policy,
+                          int64_t deadline_ns, int threads, int32_t* sigma_out, int32_t* tau_out,
+                          orc_stats* stats, int64_t* trace_switch, double* trace_value,
+                          int64_t trace_cap, int64_t* trace_len);
+
+/* Greedy assignment rule of lsapgpu_greedy_assignment (EXTENSION, not in the
+ * reference): rounds in which every unassigned agent claims the best free job
+ * of its row (smallest job on ties) and every claimed job goes to the highest
+ * claim (smallest agent on ties).  Returns the number of rounds. */
+int64_t orc_greedy_assignment(const double* a, int32_t n, int32_t* sigma_out);
+
 /* ---- auction.cpp:12-153: the synchronous auction baseline ------------------
  * AuctionConfig (baselines.hpp:12-26): has_eps selects epsilon; scaling and
  * scale_factor as there.  expire_round < 0: no deadline; k >= 0: the deadline

@@ -110,6 +110,11 @@ class Oracle:
             _dp, C.c_int32, _ip, _ip, C.POINTER(C.c_double), _dp, _ip, _bp, _dp, _ip, _bp, _bp, _bp,
             C.c_double, _ip, _ip, _ip, _ip, _dp]
         L.orc_dgs_parallel.restype = C.c_int
+        L.orc_dgs_parallel_from.argtypes = [
+            _dp, C.c_int32, _ip, C.c_double, C.c_int, C.c_int64, C.c_int, _ip, _ip, C.POINTER(_Stats),
+            _lp, _dp, C.c_int64, C.POINTER(C.c_int64)]
+        L.orc_greedy_assignment.restype = C.c_int64
+        L.orc_greedy_assignment.argtypes = [_dp, C.c_int32, _ip]
         L.orc_auction_solve.argtypes = [_dp, C.c_int32, C.c_int, C.c_double, C.c_int, C.c_double,
                                         C.c_int64, _ip, _dp, C.POINTER(_AuctionStats)]
         L.orc_dgs_parallel.argtypes = [
@@ -205,6 +210,33 @@ class Oracle:
             raise ValueError("improvement_epsilon must be >= 0")
         if rc == 3:
             raise ValueError("benefit matrix contains a non-finite entry")
+        if rc:
+            raise RuntimeError(f"oracle failure rc={rc}")
+        tr = [(int(ts[k]), float(tv[k])) for k in range(min(tl.value, cap))] if trace else []
+        return SolveResult(sig, tau, st.value, st.outer_iterations, st.switches_applied,
+                           "deadline" if st.terminated_by else "converged", st.elapsed_ms, tr,
+                           st.inner_iterations, st.agent_scans, st.job_scans, st.pair_items)
+
+    def greedy_assignment(self, a):
+        """The device greedy-assignment rule (extension): (sigma, rounds)."""
+        a = _as(a, np.float64)
+        n = a.shape[0]
+        sig = np.empty(n, np.int32)
+        rounds = self.lib.orc_greedy_assignment(a.ravel(), n, sig)
+        return sig, int(rounds)
+
+    def dgs_parallel_from(self, a, init_sigma, eps: float = 0.0, policy: int = 0, threads: int = 0,
+                          trace: bool = True) -> SolveResult:
+        """dgs_parallel's loop from a given initial sigma (job -> agent)."""
+        a = _as(a, np.float64)
+        n = a.shape[0]
+        sig, tau = np.empty(n, np.int32), np.empty(n, np.int32)
+        st = _Stats()
+        cap = TRACE_CAP + 64 if trace else 0
+        ts, tv = np.empty(max(cap, 1), np.int64), np.empty(max(cap, 1))
+        tl = C.c_int64(0)
+        rc = self.lib.orc_dgs_parallel_from(a.ravel(), n, _as(init_sigma, np.int32), eps, policy, -1, threads,
+                                            sig, tau, C.byref(st), ts, tv, cap, C.byref(tl))
         if rc:
             raise RuntimeError(f"oracle failure rc={rc}")
         tr = [(int(ts[k]), float(tv[k])) for k in range(min(tl.value, cap))] if trace else []

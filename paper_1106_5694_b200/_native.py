@@ -28,6 +28,7 @@ EXPORTS = [
     "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_solve_dist",
     "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
     "lsapgpu_set_timeline", "lsapgpu_timeline", "lsapgpu_auction_solve",
+    "lsapgpu_greedy_assignment",
 ]
 
 
@@ -39,6 +40,8 @@ class Params(C.Structure):
         ("use_graph", C.c_int32),
         ("deadline_ns", C.c_int64),
         ("init_sigma", C.c_void_p),
+        ("init_mode", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -147,6 +150,7 @@ def _load() -> C.CDLL:
         "lsapgpu_timeline": (C.c_int32, [vp, C.c_void_p, C.c_int32]),
         "lsapgpu_auction_solve": (C.c_int, [vp, C.POINTER(AuctionParams), vp, vp, C.POINTER(AuctionStats),
                                             vp, vp, i64]),
+        "lsapgpu_greedy_assignment": (C.c_int, [vp, vp, C.POINTER(i64)]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
                                           C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),
     }

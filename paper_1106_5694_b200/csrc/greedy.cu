@@ -1,0 +1,197 @@
+// greedy.cu -- greedy initial assignment on the device (BASELINE north star
+// item 2; an EXTENSION: the reference's dgs_parallel always starts from
+// initial_random, dgs.cpp:22-25, so solves from this start are checked against
+// the oracle's restatement of the same loop, not against the reference).
+//
+// Deterministic claim rounds: every unassigned agent takes the argmax of its
+// row over the still-free jobs (smallest job on ties); each claimed job goes
+// to the highest claim (smallest agent on ties) through one 128-bit CAS on a
+// {inverted agent, order-preserving benefit key} slot; losers retry next
+// round on the remaining jobs.  Every claimed job has a winner, so each round
+// assigns at least one agent (C1-C3: ~10 rounds).  One cooperative launch:
+// rounds are separated by grid-wide barriers; the free-job bitmap is staged
+// into every CTA's shared memory at the start of a round, and rows are read
+// as 16-byte vectors by one warp per agent.
+#include <cooperative_groups.h>
+
+#include <climits>
+
+#include "state.h"
+
+namespace cg = cooperative_groups;
+
+namespace lsapgpu {
+namespace {
+
+constexpr int kGT = 512;
+
+__device__ __forceinline__ unsigned long long gkey(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ void gcas128(unsigned long long* p, unsigned long long c0, unsigned long long c1,
+                                        unsigned long long s0, unsigned long long s1, unsigned long long& o0,
+                                        unsigned long long& o1) {
+  asm volatile(
+      "{\n\t.reg .b128 d, c, s;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 s, {%4, %5};\n\t"
+      "atom.relaxed.gpu.global.cas.b128 d, [%6], c, s;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(o0), "=l"(o1)
+      : "l"(c0), "l"(c1), "l"(s0), "l"(s1), "l"(p)
+      : "memory");
+}
+
+// Keep the lexicographic maximum of {benefit key, inverted agent} in a slot.
+__device__ __forceinline__ void post_claim(unsigned long long* slot, double v, int32_t agent) {
+  const unsigned long long h = gkey(v), l = 0xFFFFFFFFull - static_cast<unsigned long long>(agent);
+  unsigned long long c0 = 0, c1 = 0;
+  for (;;) {
+    if (c1 > h || (c1 == h && c0 >= l)) return;
+    unsigned long long o0, o1;
+    gcas128(slot, c0, c1, l, h, o0, o1);
+    if (o0 == c0 && o1 == c1) return;
+    c0 = o0;
+    c1 = o1;
+  }
+}
+
+template <class E>
+__global__ void __launch_bounds__(kGT) greedy_kernel(DevState st, GreedyDev g) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint32_t s_free[];  // free-job bitmap of the round
+  const int32_t n = st.n;
+  const int64_t ld = st.ld;
+  const E* A = static_cast<const E*>(st.A);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kGT + tid;
+  const int64_t gthreads = static_cast<int64_t>(gridDim.x) * kGT;
+  const int32_t gwarp = blockIdx.x * (kGT / 32) + warp, nwarps = gridDim.x * (kGT / 32);
+  const int32_t words = (n + 31) / 32;
+  constexpr int VE = 16 / sizeof(E);
+
+  for (int64_t x = gtid; x < n; x += gthreads) {
+    g.list[0][x] = static_cast<int32_t>(x);
+    st.sigma[x] = -1;
+  }
+  for (int64_t w = gtid; w < words; w += gthreads)
+    g.free[w] = (w == words - 1 && (n & 31)) ? ((1u << (n & 31)) - 1u) : 0xFFFFFFFFu;
+  if (gtid == 0) {
+    g.ctrl->count[0] = n;
+    g.ctrl->count[1] = 0;
+    g.ctrl->rounds = 0;
+  }
+  grid.sync();
+  int cur = 0;
+  for (;;) {
+    const int32_t cnt = __ldcg(&g.ctrl->count[cur]);
+    if (cnt == 0) break;
+    for (int32_t w = tid; w < words; w += kGT) s_free[w] = __ldcg(g.free + w);
+    __syncthreads();
+    const int32_t* list = cur ? g.list[1] : g.list[0];
+    int32_t* next = cur ? g.list[0] : g.list[1];
+
+    // ---- claim: one warp per agent, best free job of its row ----
+    for (int32_t k = gwarp; k < cnt; k += nwarps) {
+      const int32_t i = __ldcg(list + k);
+      const uint4* rv = reinterpret_cast<const uint4*>(A + static_cast<int64_t>(i) * ld);
+      double bv = -__longlong_as_double(0x7FF0000000000000ll);
+      int32_t bj = INT_MAX;
+      for (int32_t v = lane; v * VE < n; v += 32) {
+        const uint32_t fw = s_free[(v * VE) >> 5] >> ((v * VE) & 31);
+        if ((fw & ((1u << VE) - 1u)) == 0u) continue;  // no free job in this vector
+        const uint4 w = __ldg(rv + v);
+        const E* e = reinterpret_cast<const E*>(&w);
+#pragma unroll
+        for (int q = 0; q < VE; ++q) {
+          const int32_t j = v * VE + q;
+          if (j < n && ((fw >> q) & 1u)) {
+            const double x = static_cast<double>(e[q]);
+            if (x > bv) {  // ascending j per lane: strict > keeps the first
+              bv = x;
+              bj = j;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, off);
+        if (ov > bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      if (lane == 0) {
+        g.claim[i] = bj;
+        post_claim(g.slot + 2 * static_cast<int64_t>(bj), bv, i);
+      }
+    }
+    grid.sync();
+
+    // ---- award: the slot's agent takes the job, the others retry ----
+    for (int64_t base = gtid - lane; base < cnt; base += gthreads) {
+      const int64_t k = base + lane;
+      bool lost = false;
+      int32_t i = -1;
+      if (k < cnt) {
+        i = __ldcg(list + k);
+        const int32_t j = __ldcg(g.claim + i);
+        unsigned long long* sl = g.slot + 2 * static_cast<int64_t>(j);
+        if (static_cast<int32_t>(0xFFFFFFFFull - __ldcg(sl)) == i) {
+          st.sigma[j] = i;
+          atomicAnd(g.free + (j >> 5), ~(1u << (j & 31)));
+          sl[0] = 0ull;
+          sl[1] = 0ull;
+        } else {
+          lost = true;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, lost);
+      if (m) {
+        int b0 = 0;
+        if (lane == 0) b0 = atomicAdd(&g.ctrl->count[cur ^ 1], __popc(m));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (lost) next[b0 + __popc(m & ((1u << lane) - 1))] = i;
+      }
+    }
+    if (gtid == 0) {
+      g.ctrl->count[cur] = 0;  // every thread read it at the top of this round
+      g.ctrl->rounds += 1;
+    }
+    grid.sync();
+    cur ^= 1;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_greedy(const DevState& d, const GreedyDev& g, int num_sms, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>((d.n + 31) / 32) * 4;
+  void* args[2];
+  DevState dd = d;
+  GreedyDev gg = g;
+  args[0] = &dd;
+  args[1] = &gg;
+  auto go = [&](const void* k) -> cudaError_t {
+    int per_sm = 0;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kGT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    return cudaLaunchCooperativeKernel(k, dim3(num_sms * per_sm), dim3(kGT), args, smem, st);
+  };
+  switch (d.storage) {
+    case kI16: return go(reinterpret_cast<const void*>(greedy_kernel<int16_t>));
+    case kI32: return go(reinterpret_cast<const void*>(greedy_kernel<int32_t>));
+    case kF32: return go(reinterpret_cast<const void*>(greedy_kernel<float>));
+    case kF64: return go(reinterpret_cast<const void*>(greedy_kernel<double>));
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace lsapgpu

@@ -200,6 +200,9 @@ struct lsapgpu_ctx {
   uint64_t perm_seed = 0;
   Ctrl* ctrl_base = nullptr;
 
+  GreedyDev gr;                    // greedy assignment scratch (per n, in vec_bufs)
+  int32_t gr_n = 0;
+
   AuctionDev au;
   int32_t au_n = 0;
   AuctionCtrl* au_host = nullptr;  // pinned
@@ -242,6 +245,7 @@ void free_vectors(lsapgpu_ctx* ctx) {
   ctx->vec_bufs.clear();
   ctx->n_vec = 0;
   ctx->au_n = 0;
+  ctx->gr_n = 0;
 }
 
 template <class T>
@@ -568,6 +572,25 @@ int device_objective(lsapgpu_ctx* ctx, double* value) {
   double sum = 0.0;
   for (int32_t j = 0; j < n; ++j) sum += hv[j];
   *value = sum;
+  return LSAPGPU_OK;
+}
+
+// Greedy assignment (greedy.cu) into d.sigma on the context's stream.
+int run_greedy(lsapgpu_ctx* ctx) {
+  DevState& d = ctx->d;
+  GreedyDev& g = ctx->gr;
+  if (ctx->gr_n != d.n) {
+    const size_t N = static_cast<size_t>(d.ld);
+    CK(valloc(ctx, &g.list[0], N, false));
+    CK(valloc(ctx, &g.list[1], N, false));
+    CK(valloc(ctx, &g.free, N / 32 + 1, false));
+    CK(valloc(ctx, &g.claim, N, false));
+    CK(valloc(ctx, &g.slot, 2 * N, true));  // empty slots; every award resets its slot
+    CK(valloc(ctx, &g.ctrl, 1, true));
+    ctx->gr_n = d.n;
+  }
+  CK(launch_greedy(d, g, ctx->num_sms, ctx->stream));
+  ++ctx->launches;
   return LSAPGPU_OK;
 }
 
@@ -1129,9 +1152,14 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
 
   // initial permutation: random_perm(seed) is sequential by nature and a pure
   // function of (n, seed), so the last one is kept in pinned memory
+  if (P.init_mode != LSAPGPU_INIT_RANDOM && P.init_mode != LSAPGPU_INIT_GREEDY)
+    return fail(ctx, LSAPGPU_ERR_INVALID, "unknown init mode");
   if (P.init_sigma) {
     if (!is_perm(P.init_sigma, n)) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid assignment: not a permutation");
     CK(cpy(ctx, d.sigma, P.init_sigma, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  } else if (P.init_mode == LSAPGPU_INIT_GREEDY) {
+    int grc = run_greedy(ctx);
+    if (grc) return grc;
   } else {
     if (ctx->perm_n != n || ctx->perm_seed != P.seed) {
       CK(cudaStreamSynchronize(ctx->stream));  // a previous upload may still read the buffer
@@ -1505,5 +1533,20 @@ int lsapgpu_auction_solve(lsapgpu_ctx* ctx, const lsapgpu_auction_params* params
     stats->bytes_scanned = H.bids * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage) + 8);
     stats->storage = d.storage;
   }
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_greedy_assignment(lsapgpu_ctx* ctx, int32_t* sigma_out, int64_t* rounds) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (!ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  if (!sigma_out) return fail(ctx, LSAPGPU_ERR_INVALID, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  int rc = run_greedy(ctx);
+  if (rc) return rc;
+  GreedyCtrl gc;
+  CK(cpy(ctx, sigma_out, ctx->d.sigma, sizeof(int32_t) * ctx->n_matrix, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cpy(ctx, &gc, ctx->gr.ctrl, sizeof(gc), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (rounds) *rounds = gc.rounds;
   return LSAPGPU_OK;
 }

@@ -206,4 +206,19 @@ cudaError_t launch_auction(const DevState& d, const AuctionDev& a, int64_t remai
 cudaError_t launch_minmax(const DevState& d, AuctionCtrl* c, cudaStream_t st);
 double auction_key_value(unsigned long long key);
 
+// greedy.cu (greedy initial assignment; extension, see the file header)
+struct GreedyCtrl {
+  int32_t count[2];
+  int64_t rounds;
+};
+struct GreedyDev {
+  int32_t* list[2] = {nullptr, nullptr};  // unassigned agents (ping-pong)
+  uint32_t* free = nullptr;               // free-job bitmap
+  int32_t* claim = nullptr;               // per agent: the job it claims this round
+  unsigned long long* slot = nullptr;     // per job: {inverted agent, benefit key} of the best claim
+  GreedyCtrl* ctrl = nullptr;
+};
+// sigma (device) = the greedy assignment of the matrix in d
+cudaError_t launch_greedy(const DevState& d, const GreedyDev& g, int num_sms, cudaStream_t st);
+
 }  // namespace lsapgpu

@@ -153,8 +153,11 @@ class ParallelConfig:
     reeval: str = "touched_and_conflicted"  # or "touched_only"
     device: int = 0
     use_graph: bool = True
+    init: str = "random"  # extension: "greedy" starts from the device greedy assignment
 
     def validate(self) -> None:
+        if self.init not in ("random", "greedy"):
+            raise Error(f"unknown init '{self.init}'")
         if not (self.improvement_epsilon >= 0.0):
             raise Error("improvement_epsilon must be >= 0")
         if self.workers < 0:
@@ -369,6 +372,7 @@ class Context:
         p.reeval = 0 if cfg.reeval == "touched_and_conflicted" else 1
         p.use_graph = 1 if cfg.use_graph else 0
         p.deadline_ns = -1 if cfg.deadline is None else int(cfg.deadline)
+        p.init_mode = 1 if getattr(cfg, "init", "random") == "greedy" else 0
         if init_sigma is not None:
             init_sigma = np.ascontiguousarray(init_sigma, np.int32)
             p.init_sigma = init_sigma.ctypes.data
@@ -401,6 +405,14 @@ class Context:
         rep.gpu["storage"] = N.STORAGE_NAMES[st.storage]
         rep.gpu["trace_len"] = tl.value
         return rep
+
+    def greedy_assignment(self):
+        """Greedy assignment of this context's matrix (extension; see
+        lsapgpu_greedy_assignment): (sigma, claim rounds)."""
+        sigma = np.empty(self.n, np.int32)
+        rounds = C.c_int64(0)
+        self._check(N.LIB.lsapgpu_greedy_assignment(self.h, N.ptr(sigma), C.byref(rounds)))
+        return sigma, rounds.value
 
     def auction_solve(self, cfg: Optional["AuctionConfig"] = None, on_round=None,
                       round_cap: int = 4096) -> SolveReport:
