@@ -173,6 +173,17 @@ int main() {
       CHECK(cut.terminated_by == Termination::deadline);
       validate_assignment(inst, cut.assignment);
     }
+    // greedy start (extension): a valid, deterministic assignment
+    {
+      gpu::GpuConfig c;
+      c.greedy_init = true;
+      const Instance inst = random_int_instance(700, 31, 1000);
+      const auto r1 = gpu::dgs_parallel(inst, c);
+      const auto r2 = gpu::dgs_parallel(inst, c);
+      validate_assignment(inst, r1.assignment);
+      CHECK(r1.assignment.sigma == r2.assignment.sigma && r1.assignment.value == r2.assignment.value);
+      CHECK(r1.assignment.value == objective(inst, r1.assignment));
+    }
     // auction_solve, bit for bit (test_baselines.cpp:62-160 instances + C1/P2P)
     {
       auto auction_both = [](const Instance& inst, const AuctionConfig& cfg) {
