@@ -180,6 +180,7 @@ struct lsapgpu_ctx {
   int32_t obj_cap = 0;
   LogEntry* log_pin = nullptr;   // delta-log prefix drained with the control block
   static constexpr int64_t kLogPin = 1 << 16;
+  int64_t log_hint[4] = {kLogPin, kLogPin, kLogPin, kLogPin};  // log entries per outer pass, last solve
 
   // host upload pipeline (lsapgpu_set_matrix)
   cudaStream_t copy_stream = nullptr;
@@ -1237,6 +1238,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   int64_t launches = 0;
   int64_t graph_launches = 0;
   bool prefetched = false;  // ctrl + log prefix already read back with the graph's sync
+  int64_t pin_len = 0;      // entries of that prefix
 
   while (!expired) {
     ++S.outer_iterations;
@@ -1273,8 +1275,12 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         ++graph_launches;
         // control block and the first kLogPin log entries with one sync
         CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cpy(ctx, ctx->log_pin, d.log, sizeof(LogEntry) * std::min<int64_t>(lsapgpu_ctx::kLogPin, d.log_cap),
-               cudaMemcpyDeviceToHost, ctx->stream));
+        // log prefix sized from what this pass produced in the previous solve
+        // (bench steps repeat a solve): the rest, if any, follows with a sync
+        const int hp = std::min<int>(static_cast<int>(S.outer_iterations) - 1, 3);
+        pin_len = std::min<int64_t>(std::min<int64_t>(lsapgpu_ctx::kLogPin, d.log_cap),
+                                    ctx->log_hint[hp] + ctx->log_hint[hp] / 4 + 1024);
+        CK(cpy(ctx, ctx->log_pin, d.log, sizeof(LogEntry) * pin_len, cudaMemcpyDeviceToHost, ctx->stream));
         hmark("graph launched");
         CK(cudaStreamSynchronize(ctx->stream));
         hmark("graph done");
@@ -1310,7 +1316,8 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
       }
       const int64_t cnt = C.log_count;
-      const int64_t have = prefetched ? std::min<int64_t>(cnt, lsapgpu_ctx::kLogPin) : 0;
+      const int64_t have = prefetched ? std::min<int64_t>(cnt, pin_len) : 0;
+      if (!C.drain) ctx->log_hint[std::min<int>(static_cast<int>(S.outer_iterations) - 1, 3)] = cnt;
       // Replay in the reference's batch order (iteration, then ascending slot:
       // agents then jobs, parallel.cpp:306-310).  Integer deltas sum exactly in
       // any order, so without a trace the order only matters for float storage.
