@@ -106,6 +106,13 @@ __device__ __forceinline__ unsigned long long now_ns() {
   return t;
 }
 
+__device__ __forceinline__ void row_pf(const void* p, uint32_t bytes) {
+  for (uint32_t off = 0; off < bytes; off += 32768u)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const char*>(p) + off),
+                 "r"(bytes - off < 32768u ? bytes - off : 32768u)
+                 : "memory");
+}
+
 // 128-bit compare-and-swap on a bid slot {lo, hi}; returns the old value.
 __device__ __forceinline__ void cas128(unsigned long long* p, unsigned long long c0, unsigned long long c1,
                                        unsigned long long s0, unsigned long long s1, unsigned long long& o0,
@@ -323,6 +330,12 @@ __global__ void __launch_bounds__(kNT, 1) auction_kernel(DevState st, AuctionDev
           int32_t* seg = next + static_cast<int64_t>(rank) * n;
           if (lost) seg[b0 + __popc(ml & ((1u << lane) - 1))] = i;
           if (displaced) seg[b0 + __popc(ml) + __popc(md & ((1u << lane) - 1))] = prev;
+          // next round's rows start streaming into L2 now (matrices larger than L2)
+          if (a.row_prefetch) {
+            const uint32_t rb = static_cast<uint32_t>(static_cast<size_t>(n) * sizeof(E) + 15) / 16 * 16;
+            if (lost) row_pf(A + static_cast<int64_t>(i) * ld, rb);
+            if (displaced) row_pf(A + static_cast<int64_t>(prev) * ld, rb);
+          }
         }
       }
       for (int off = 16; off > 0; off >>= 1) awards += __shfl_down_sync(0xffffffffu, awards, off);

@@ -194,6 +194,7 @@ struct AuctionDev {
   double* rec_bid = nullptr;
   int32_t* wl[2] = {nullptr, nullptr};  // bidder lists, one n-entry segment per cluster CTA
   int local_prices = 0;         // 1: every CTA holds a shared-memory replica of the prices
+  int row_prefetch = 0;         // 1: L2-prefetch the rows of the next round's bidders
   AuctionCtrl* ctrl = nullptr;
   const double* eps_list = nullptr;  // epsilon of every phase (host-computed schedule)
   int32_t n_eps = 0;
