@@ -412,3 +412,46 @@ def test_errors_match_reference_messages():
     ctx = g.context(0)
     with pytest.raises(g.Error, match="non-finite"):
         ctx.set_matrix(np.array([[1.0, np.inf], [0.0, 1.0]]))
+
+
+def _solve_vs_oracle(oracle, gpu_ctx, a, seed=0, **kw):
+    gpu_ctx.set_matrix(a)
+    rep = gpu_ctx.solve(_g().ParallelConfig(seed=seed, **kw))
+    assert_same_solve(rep, oracle.dgs_parallel(a, seed=seed))
+    return rep
+
+
+@pytest.mark.parametrize("n", [63, 65, 129])
+def test_dgs_ragged_sizes(oracle, gpu_ctx, n):
+    _solve_vs_oracle(oracle, gpu_ctx, oracle.generate("int", n, n, 1000.0), seed=n)
+
+
+def test_dgs_negative_integers(oracle, gpu_ctx):
+    a = oracle.generate("int", 700, 21, 2000.0) - 1000.0  # int16 storage with negatives
+    rep = _solve_vs_oracle(oracle, gpu_ctx, a, seed=4)
+    assert rep.gpu["storage"] == "int16"
+
+
+def test_dgs_constant_matrix_no_switch(oracle, gpu_ctx):
+    a = np.full((300, 300), 5.0)
+    rep = _solve_vs_oracle(oracle, gpu_ctx, a, seed=1)
+    assert rep.switches_applied == 0 and rep.outer_iterations == 1
+
+
+@pytest.mark.parametrize("hi,storage", [(536870911.0, "int32"), (536870912.0 * 4, "fp64")])
+def test_dgs_storage_boundaries(oracle, gpu_ctx, hi, storage):
+    """Integers up to 2^29 - 1 stay int32; beyond, the exact fp64 path."""
+    a = np.floor(oracle.generate("unit", 400, 33, 1.0) * hi)
+    rep = _solve_vs_oracle(oracle, gpu_ctx, a, seed=2)
+    assert rep.gpu["storage"] == storage
+
+
+@pytest.mark.parametrize("n", [16384, 16385])
+def test_dgs_key_mode_boundary(oracle, gpu_ctx, n):
+    """Packed 32-bit keys up to n = 16384, 64-bit keys beyond (same results)."""
+    gpu_ctx.generate("int", n, 3, 1000.0)
+    rep = gpu_ctx.solve(_g().ParallelConfig(seed=1), trace=False)
+    a = oracle.generate("int", n, 3, 1000.0)
+    want = oracle.dgs_parallel(a, seed=1, trace=False)
+    assert np.array_equal(rep.assignment.sigma, want.sigma)
+    assert rep.assignment.value == want.value and rep.switches_applied == want.switches_applied
