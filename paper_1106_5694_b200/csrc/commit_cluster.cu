@@ -64,6 +64,7 @@ struct CommitScratch {  // per-CTA shared scalars
   int nlog, nconf, nconf_j;
   unsigned long long base_log;
   int base_items;
+  int base_conf;
 };
 
 // Per-proposal working set of this CTA (shared memory, or global scratch
@@ -200,20 +201,37 @@ __global__ void __launch_bounds__(kNT, 1)
     Ea.slot = st.c_jnew + e0;
     Ea.st = st.estate + e0;
   }
-  for (int32_t l = tid; l < cnt; l += kNT) {
-    // proposals carry {slot, proposer, partner, job}: one dependent load left
-    const int4 en = prop_key(edges[e0 + l], n);
-    Ea.u[l] = en.y;  // proposer: the agent, or the job's current holder (frozen)
-    if (en.x < n) {
-      Ea.v[l] = st.sigma[en.z];  // the displaced holder of the proposed job
-      Ea.jold[l] = en.w;         // the proposer's current job
-    } else {
-      Ea.v[l] = en.z;             // the proposed agent
-      Ea.jold[l] = st.tau[en.z];  // ... and its current job
+  if (st.policy == 0) {
+    // default policy: every proposal was written by this batch's scan on the
+    // frozen state, so it carries both endpoints (commit_single.cuh header)
+    for (int32_t l = tid; l < cnt; l += kNT) {
+      const Prop* pe = edges + e0 + l;
+      const int4 h = *reinterpret_cast<const int4*>(pe);  // slot, a, d, j_new
+      const bool agent_rec = h.x < n;
+      Ea.u[l] = agent_rec ? h.y : h.z;  // proposer: the agent, or the job's holder
+      Ea.v[l] = agent_rec ? h.z : h.y;  // the displaced holder / the proposed agent
+      Ea.jold[l] = pe->j_old;
+      Ea.st[l] = kEdgeUndecided;
+      Ea.rank[l] = kNoEmit;
+      Ea.slot[l] = h.x;
     }
-    Ea.st[l] = kEdgeUndecided;
-    Ea.rank[l] = kNoEmit;
-    Ea.slot[l] = en.x;
+  } else {
+    // touched_only: records may predate this batch; endpoints from the
+    // current assignment, as check_conflicts reads them (parallel.cpp:35-76)
+    for (int32_t l = tid; l < cnt; l += kNT) {
+      const int4 en = prop_key(edges[e0 + l], n);
+      Ea.u[l] = en.y;  // proposer: the agent, or the job's current holder (frozen)
+      if (en.x < n) {
+        Ea.v[l] = st.sigma[en.z];  // the displaced holder of the proposed job
+        Ea.jold[l] = en.w;         // the proposer's current job
+      } else {
+        Ea.v[l] = en.z;             // the proposed agent
+        Ea.jold[l] = st.tau[en.z];  // ... and its current job
+      }
+      Ea.st[l] = kEdgeUndecided;
+      Ea.rank[l] = kNoEmit;
+      Ea.slot[l] = en.x;
+    }
   }
   cluster.sync();
   if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 11);
@@ -293,6 +311,9 @@ __global__ void __launch_bounds__(kNT, 1)
     // Default policy: every proposal is fresh (commit_single.cuh), so
     // committed == accepted and touched == matched; classify here and let
     // commit_apply_kernel do the scattered writes grid-wide.
+    // Each CTA ranks its edges in shared memory and reserves its range of
+    // the committed / queued lists with ONE global atomic (per-warp global
+    // atomics on the two counters serialised ~600 deep at L2).
     const int lane = tid & 31;
     for (int32_t base = tid - lane; base < cnt; base += kNT) {
       const int32_t l = base + lane;
@@ -301,17 +322,23 @@ __global__ void __launch_bounds__(kNT, 1)
       const unsigned am = __ballot_sync(0xffffffffu, acc);
       if (am) {
         int r0 = 0;
-        if (lane == 0) r0 = atomicAdd(&C->k2_nlog, __popc(am));
+        if (lane == 0) r0 = atomicAdd(&sc.nlog, __popc(am));
         r0 = __shfl_sync(0xffffffffu, r0, 0);
-        if (acc) st.clist[r0 + __popc(am & ((1u << lane) - 1))] = e0 + l;
+        if (acc) Ea.rank[l] = r0 + __popc(am & ((1u << lane) - 1));
       }
       if (s == kEdgeRejected && Ea.slot[l] >= n) {
         const int32_t j = Ea.slot[l] - n;
         atomicOr(&st.jbits[j >> 5], 1u << (j & 31));
       }
     }
-    cluster.sync();  // bitmap and committed list complete
+    __syncthreads();
+    if (tid == 0) sc.base_items = sc.nlog ? atomicAdd(&C->k2_nlog, sc.nlog) : 0;
+    __syncthreads();
+    for (int32_t l = tid; l < cnt; l += kNT)
+      if (Ea.st[l] == kEdgeAccepted) st.clist[sc.base_items + Ea.rank[l]] = e0 + l;
     if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 14);
+    // conflicted proposers: unmatched owners of rejected records, queued once
+    // (the matched keys are final since the last LFMM barrier)
     for (int32_t base = tid - lane; base < cnt; base += kNT) {
       const int32_t l = base + lane;
       bool q = false;
@@ -322,14 +349,22 @@ __global__ void __launch_bounds__(kNT, 1)
       const unsigned qm = __ballot_sync(0xffffffffu, q);
       if (qm) {
         int r0 = 0;
-        if (lane == 0) r0 = atomicAdd(&C->k2_nconf, __popc(qm));
+        if (lane == 0) r0 = atomicAdd(&sc.nconf, __popc(qm));
         r0 = __shfl_sync(0xffffffffu, r0, 0);
-        if (q) st.qlist[r0 + __popc(qm & ((1u << lane) - 1))] = e0 + l;
+        if (q) Ea.rank[l] = r0 + __popc(qm & ((1u << lane) - 1));
+        else if (l < cnt && Ea.st[l] == kEdgeRejected) Ea.rank[l] = kNoEmit;
+      } else if (l < cnt && Ea.st[l] == kEdgeRejected) {
+        Ea.rank[l] = kNoEmit;
       }
     }
+    __syncthreads();
+    if (tid == 0) sc.base_conf = sc.nconf ? atomicAdd(&C->k2_nconf, sc.nconf) : 0;
+    __syncthreads();
+    for (int32_t l = tid; l < cnt; l += kNT)
+      if (Ea.st[l] == kEdgeRejected && Ea.rank[l] != kNoEmit) st.qlist[sc.base_conf + Ea.rank[l]] = e0 + l;
     cluster.sync();  // counts final; peers done with this CTA's shared memory
     if (rank == 0 && tid == 0) {
-      const int nlog = C->k2_nlog, nconf = C->k2_nconf, nitems = 2 * nlog + nconf;
+      const int nlog = __ldcg(&C->k2_nlog), nconf = __ldcg(&C->k2_nconf), nitems = 2 * nlog + nconf;
       C->k2_parity = P;
       C->k2_iter = iter;
       C->k2_log_base = C->log_count;
