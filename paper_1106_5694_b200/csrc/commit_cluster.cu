@@ -129,13 +129,13 @@ __global__ void __launch_bounds__(kNT, 1)
   // (commit_single.cuh).  Otherwise the whole cluster runs the iteration.
   if (m <= cta_cap && (st.policy == 0 || mode == kCommitCheckOnly)) {
     if (m <= kSingleLoad) {  // few proposals: rank 0 loads them itself
-      if (rank == 0) single::commit_single(st, mode, cta_cap, smem);
+      if (rank == 0) single::commit_single(st, mode, cta_cap, smem, false, !(var & 2));
     } else {  // many: every rank loads a share straight into rank 0's shared memory
       unsigned char* dst = cluster.map_shared_rank(smem, 0);
       const int32_t per = (m + CS - 1) / CS;
       single::load_share(st, cta_cap, dst, min(m, rank * per), min(m, (rank + 1) * per));
       cluster.sync();
-      if (rank == 0) single::commit_single(st, mode, cta_cap, smem, true);
+      if (rank == 0) single::commit_single(st, mode, cta_cap, smem, true, !(var & 2));
     }
     if (mode == kCommitSolve && fused) {  // the batch's scattered writes, cluster-wide
       cluster.sync();

@@ -64,7 +64,7 @@ __host__ __device__ inline int edge_capacity(int32_t n, size_t smem) {
 // slot / a / d / state of every proposal into this CTA's shared memory
 // (load_share below), otherwise the CTA loads them itself.
 __device__ __forceinline__ void commit_single(const DevState& st, int mode, int edge_cap, unsigned char* smem,
-                                              bool preloaded = false) {
+                                              bool preloaded = false, bool early_exit = true) {
   const int tid = threadIdx.x;
   __shared__ Scratch sc;
 
@@ -121,20 +121,33 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
       }
     }
     if (__syncthreads_or(local) == 0) break;
+    int live = 0;
     for (int32_t l = tid; l < m; l += kNT) {
       if (Est[l] != kEdgeUndecided) continue;
       const int32_t u = Ea[l], v = Ed[l];
       const uint32_t k = make_key(R, Eslot[l]);
-      if (keys[u] == k && keys[v] == k) {
+      const uint32_t ku = keys[u], kv = keys[v];
+      if (ku == k && kv == k) {
         Est[l] = kEdgeAccepted;
         keys[u] = kMatched;
         keys[v] = kMatched;
+      } else if (ku != kMatched && kv != kMatched) {
+        live = 1;  // may still be accepted (an endpoint not seen matched yet)
       }
     }
-    __syncthreads();
-    if (tid == 0) tl_mark(C, st.tl, st.tl_cap, 6);
     ++R;
     ++rounds;
+    // every edge still undecided has an endpoint seen matched (matching is
+    // permanent): the next round would only reject them, so do that here and
+    // skip its posting pass and barrier
+    const bool done = __syncthreads_or(live || !early_exit) == 0;
+    if (tid == 0) tl_mark(C, st.tl, st.tl_cap, 6);
+    if (done) {
+      for (int32_t l = tid; l < m; l += kNT)
+        if (Est[l] == kEdgeUndecided) Est[l] = kEdgeRejected;
+      __syncthreads();
+      break;
+    }
   }
 
   if (mode == kCommitCheckOnly) {  // step API: per-proposal state, proposer first
