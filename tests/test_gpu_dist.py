@@ -94,3 +94,18 @@ def test_torch_distributed_two_ranks(oracle, gpu_ctx, tmp_path):
     for rank in range(2):
         sig = np.load(tmp_path / f"sigma{rank}.npy")
         assert np.array_equal(sig, ref.assignment.sigma)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_greedy_start(oracle, gpu_ctx, world):
+    """Every rank computes the same (deterministic) greedy start on its replica."""
+    import paper_1106_5694_b200 as g
+    a = oracle.generate("p2p", 1200, 7)
+    cfg = g.ParallelConfig(init="greedy")
+    gpu_ctx.set_matrix(a)
+    ref = gpu_ctx.solve(cfg)
+    reps, _ = solve_ranks(a, cfg, world)
+    for rep in reps:
+        assert np.array_equal(rep.assignment.sigma, ref.assignment.sigma)
+        assert rep.assignment.value == ref.assignment.value
+        assert rep.objective_trace == ref.objective_trace
