@@ -200,7 +200,7 @@ cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
                           cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st) {
   if (mode == kCommitApplyOnly) return cudaErrorInvalidValue;  // launch_accepted_from_masks
   cudaError_t e = launch_commit_cluster(d, p, mode, cond, use_cond, st);
-  if (e != cudaSuccess || mode != kCommitSolve || p.fused_apply) return e;
+  if (e != cudaSuccess || mode != kCommitSolve || p.fused_apply || d.fuse_apply) return e;
   return launch_commit_apply(d, st);
 }
 

@@ -105,6 +105,8 @@ struct Ctrl {
   // commit_apply): committed / queued-conflicted proposal lists of one batch
   int32_t k2_parity, k2_nlog, k2_nconf, k2_iter;
   int64_t k2_log_base;
+  // grid barrier of the resident scan when it runs the batch's apply itself
+  uint32_t gbar_count, gbar_gen;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

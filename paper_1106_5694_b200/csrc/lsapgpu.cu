@@ -75,6 +75,7 @@ constexpr int kRing = 3;                       // pinned bounce buffers (pageabl
 constexpr size_t kStageKeep = 16ull << 30;     // keep the device staging copy up to this size
 
 int upload_threads() {
+  if (const char* e = std::getenv("LSAPGPU_UPLOAD_THREADS")) return std::max(1, std::atoi(e));
   const unsigned hw = std::thread::hardware_concurrency();
   return static_cast<int>(std::max(2u, std::min(8u, hw ? hw / 2 : 2u)));
 }
@@ -1218,6 +1219,14 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
 
   d.eps = P.eps;
   d.policy = P.reeval;
+  // single GPU + resident scan: LSAPGPU_FUSE_APPLY=1 lets the scan run each
+  // batch's apply itself behind a grid barrier instead of commit_apply_kernel
+  // (opt-in: measured 5 % slower at C3 -- the barrier waits for the CTAs the
+  // commit cluster's SMs delay, where PDL overlaps the small apply kernel)
+  {
+    static const bool fuse_env = std::getenv("LSAPGPU_FUSE_APPLY") && std::atoi(std::getenv("LSAPGPU_FUSE_APPLY"));
+    d.fuse_apply = (!multi && ctx->scan_plan.resident && fuse_env) ? 1 : 0;
+  }
   if (!expired) {
     set_deadline_kernel<<<1, 1, 0, ctx->stream>>>(
         ctx->ctrl_dev, P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns()));
@@ -1297,7 +1306,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
             ctx->commit_ms += cms;
             ++ctx->commit_launches;
           }
-          ctx->launches += ctx->commit_plan.launches();  // conflict check (+ apply)
+          ctx->launches += d.fuse_apply ? 1 : ctx->commit_plan.launches();  // conflict check (+ apply)
           rc = run_scan(ctx, 0);
           if (rc) return rc;
           ++launches;
@@ -1401,7 +1410,8 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   // every body pass of the graph is a commit (conflict check + apply) and a
   // scan launch; the last pass per graph launch finds no active record and
   // exits early
-  if (graphed) ctx->launches += (1 + ctx->commit_plan.launches()) * (S.inner_iterations + graph_launches);
+  if (graphed)
+    ctx->launches += (1 + (d.fuse_apply ? 1 : ctx->commit_plan.launches())) * (S.inner_iterations + graph_launches);
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 

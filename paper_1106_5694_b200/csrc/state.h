@@ -73,6 +73,7 @@ struct DevState {
   int use_own = 0;
   int emit_edges = 1;
   int pdl = 0;  // launch the inner-loop kernels with programmatic dependent launch
+  int fuse_apply = 0;  // the resident scan runs the previous commit's apply (no commit_apply_kernel)
   // device timeline (instrumentation): CTA 0 of every scan / commit launch
   // appends (%globaltimer << 4 | kind); null when disabled
   unsigned long long* tl = nullptr;
