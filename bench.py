@@ -220,9 +220,7 @@ def run_ours(args, wl) -> None:
     cfg = g.ParallelConfig(seed=0)
     stream = torch.cuda.ExternalStream(ctx.stream)
     exch = None
-    if sharded:
-        from paper_1106_5694_b200.dist import TorchDistExchange
-        exch = TorchDistExchange()
+    transport = None
 
     def solve():
         return ctx.solve(cfg, trace=False, dist=exch)
@@ -236,6 +234,24 @@ def run_ours(args, wl) -> None:
         a_host = None
     a_dev = a_host.to(f"cuda:{local}") if a_host is not None else None
     torch.cuda.synchronize()
+    if sharded:
+        from paper_1106_5694_b200.dist import TorchDistExchange, TorchPeerExchange
+        if a_dev is not None:
+            ctx.set_matrix(a_dev)  # exchange buffers are sized for n
+        if args.exchange == "p2p":
+            # peer-memory transport: the pack kernel stores the records into
+            # every replica over NVLink (CUDA IPC mappings); NCCL if it cannot
+            # be set up on this node
+            try:
+                exch = TorchPeerExchange()
+                exch.struct(ctx)
+                transport = "peer-memory push (pack + allgather in one kernel, CUDA IPC over NVLink)"
+            except Exception as e:  # noqa: BLE001
+                exch = None
+                transport = f"nccl (peer transport unavailable: {e})"
+        if exch is None:
+            exch = TorchDistExchange()
+            transport = transport or f"{args.backend} allgather"
 
     def step_device():
         ctx.set_matrix(a_dev)
@@ -377,7 +393,7 @@ def run_ours(args, wl) -> None:
         "data": "synthetic",
         "config": {"workload": desc, "n": n, "solver_seed": 0, "reeval": "touched_and_conflicted",
                    "storage": ctx.storage,
-                   "parallelism": (f"sharded x{world}: scan items by agent index, {args.backend} record allgather, "
+                   "parallelism": (f"sharded x{world}: scan items by agent index, record exchange: {transport}, "
                                    f"replicated commit" if sharded else
                                    f"replicas x{world}" if world > 1 else "single"),
                    "l2": "inputs larger than L2 (8*n^2 B fp64 source + A/AT), no flush needed",
@@ -407,6 +423,8 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent instances instead of one sharded solve")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 sharded: record exchange over peer memory (default) or an NCCL allgather")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="N > 1 process-group backend (gloo: ranks sharing one GPU, for tests)")
     args = ap.parse_args()

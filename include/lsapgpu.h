@@ -148,9 +148,28 @@ typedef struct {
   lsapgpu_allgather_fn allgather;
   void* user;
   void* send_dev; /* >= lsapgpu_dist_exchange_bytes(n, world) bytes, device memory */
-  void* recv_dev; /* world times that */
+  void* recv_dev; /* world times that (peer mode: this rank's lsapgpu_dist_p2p_bytes buffer) */
+  /* Peer-memory transport, used instead of `allgather` when non-NULL (world
+   * <= 8): the receive buffer (lsapgpu_dist_p2p_bytes each) and the flag
+   * array (world x uint64, zeroed before the first solve) of every rank,
+   * mapped in this process (lsapgpu_ipc_open for other processes' buffers,
+   * plain pointers for ranks sharing a device).  Each rank's pack kernel
+   * stores its records straight into every replica over NVLink and raises its
+   * flag there; no collective call.  All ranks must run the same sequence of
+   * solves on these buffers. */
+  void* const* peer_recv;
+  uint64_t* const* peer_flags;
 } lsapgpu_dist;
 size_t lsapgpu_dist_exchange_bytes(int32_t n, int32_t world);
+size_t lsapgpu_dist_p2p_bytes(int32_t n, int32_t world);
+/* Zeroed device allocation of its own (cudaMalloc: the IPC handle maps the
+ * allocation base) on `device`, and its release */
+int lsapgpu_dev_alloc(int device, size_t bytes, void** dev_ptr);
+int lsapgpu_dev_free(int device, void* dev_ptr);
+/* CUDA IPC of a device allocation, as plain bytes (64-byte handle) */
+int lsapgpu_ipc_handle(const void* dev_ptr, void* handle64);
+int lsapgpu_ipc_open(const void* handle64, void** dev_ptr);
+int lsapgpu_ipc_close(void* dev_ptr);
 int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsapgpu_dist* dist,
                        int32_t* sigma_out, int32_t* tau_out, lsapgpu_stats* stats,
                        int64_t* trace_switch, double* trace_value, int64_t trace_cap,

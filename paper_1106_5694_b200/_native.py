@@ -29,6 +29,8 @@ EXPORTS = [
     "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
     "lsapgpu_set_timeline", "lsapgpu_timeline", "lsapgpu_auction_solve",
     "lsapgpu_greedy_assignment",
+    "lsapgpu_dist_p2p_bytes", "lsapgpu_ipc_handle", "lsapgpu_ipc_open", "lsapgpu_ipc_close",
+    "lsapgpu_dev_alloc", "lsapgpu_dev_free",
 ]
 
 
@@ -108,6 +110,8 @@ class Dist(C.Structure):
         ("user", C.c_void_p),
         ("send_dev", C.c_void_p),
         ("recv_dev", C.c_void_p),
+        ("peer_recv", C.POINTER(C.c_void_p)),
+        ("peer_flags", C.POINTER(C.c_void_p)),
     ]
 
 
@@ -145,6 +149,12 @@ def _load() -> C.CDLL:
         "lsapgpu_solve_dist": (C.c_int, [vp, C.POINTER(Params), C.POINTER(Dist), vp, vp, C.POINTER(Stats), vp, vp,
                                          i64, C.POINTER(i64)]),
         "lsapgpu_dist_exchange_bytes": (C.c_size_t, [i32, i32]),
+        "lsapgpu_dist_p2p_bytes": (C.c_size_t, [i32, i32]),
+        "lsapgpu_ipc_handle": (C.c_int, [vp, vp]),
+        "lsapgpu_dev_alloc": (C.c_int, [C.c_int, C.c_size_t, C.POINTER(vp)]),
+        "lsapgpu_dev_free": (C.c_int, [C.c_int, vp]),
+        "lsapgpu_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
+        "lsapgpu_ipc_close": (C.c_int, [vp]),
         "lsapgpu_set_scan_timing": (C.c_int, [vp, C.c_int]),
         "lsapgpu_set_timeline": (C.c_int, [vp, C.c_int32]),
         "lsapgpu_timeline": (C.c_int32, [vp, C.c_void_p, C.c_int32]),

@@ -107,6 +107,8 @@ struct Ctrl {
   int64_t k2_log_base;
   // grid barrier of the resident scan when it runs the batch's apply itself
   uint32_t gbar_count, gbar_gen;
+  uint32_t push_done;  // CTAs finished with the peer push of the current round
+  uint32_t pad2_;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

@@ -7,6 +7,8 @@
 // ranks apply identical batches and sigma never needs a broadcast.
 //
 // Exchange buffer per rank: 16-byte header {count} + count x Rec (32 B).
+// Two transports: the caller's allgather (e.g. NCCL) between pack and merge,
+// or the peer-memory push below (pack + allgather in one kernel).
 #include "state.h"
 
 namespace lsapgpu {
@@ -91,7 +93,82 @@ __global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t wor
   }
 }
 
+// ---- peer-memory exchange (NVLink / NVSwitch P2P) ------------------------
+// The pack step stores this rank's records straight into slot `rank` of every
+// replica's receive buffer (remote stores through peer mappings), fences at
+// system scope and raises this rank's flag in every replica to the round's
+// epoch: pack and allgather are one kernel, no collective call.  Receive
+// buffers are double-buffered by epoch parity: a rank can only be one round
+// ahead of a peer (it waits for every peer's flag before its next push), so it
+// never overwrites the buffer that peer is still merging.
+__global__ void push_kernel(DevState st, PeerSet ps, uint64_t epoch) {
+  const int32_t count = st.ctrl->own_count;
+  const size_t slot = static_cast<size_t>(epoch & 1) * ps.world * ps.bytes_per_rank +
+                      static_cast<size_t>(ps.rank) * ps.bytes_per_rank;
+  if (blockIdx.x == 0 && threadIdx.x < ps.world)
+    *reinterpret_cast<long long*>(ps.recv[threadIdx.x] + slot) = count;
+  for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+    const uint32_t w = st.items_own[k];
+    const int32_t i = static_cast<int32_t>(w & kItemMask);
+    const int32_t j = st.tau[i];
+    Rec r;
+    r.agent = (w & kItemAgent) ? i : -1;
+    r.job = (w & kItemJob) ? j : -1;
+    r.agent_partner = st.agent_partner[i];
+    r.agent_delta = st.agent_delta[i];
+    r.job_partner = st.job_partner[j];
+    r.job_delta = st.job_delta[j];
+    if (r.agent < 0) r.agent = -2 - i;
+    for (int32_t q = 0; q < ps.world; ++q) reinterpret_cast<Rec*>(ps.recv[q] + slot + 16)[k] = r;
+  }
+  // the last CTA to finish raises the flags
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&st.ctrl->push_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x < ps.world) {
+    if (threadIdx.x == 0) st.ctrl->push_done = 0;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ps.flags[threadIdx.x] + ps.rank), "l"(epoch)
+                 : "memory");
+  }
+}
+
+// One warp waits until every rank's records of this epoch have landed (lane r
+// polls rank r's flag).  10 s without progress flags an error instead of
+// hanging the device.
+__global__ void peer_wait_kernel(PeerSet ps, uint64_t epoch, Ctrl* c) {
+  const int r = threadIdx.x;
+  if (r < ps.world) {
+    const uint64_t* f = ps.flags[ps.rank] + r;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    for (;;) {
+      uint64_t v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= epoch) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) {
+        c->error = 2;
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  __syncwarp();
+}
+
 }  // namespace
+
+cudaError_t launch_dist_push(const DevState& d, const PeerSet& ps, uint64_t epoch, cudaStream_t st) {
+  push_kernel<<<148, 256, 0, st>>>(d, ps, epoch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  peer_wait_kernel<<<1, 32, 0, st>>>(ps, epoch, d.ctrl);
+  return cudaGetLastError();
+}
 
 size_t dist_exchange_bytes(int32_t n, int32_t world) {
   const size_t per = (static_cast<size_t>(n) + world - 1) / world;

@@ -202,6 +202,10 @@ struct lsapgpu_ctx {
   uint64_t perm_seed = 0;
   Ctrl* ctrl_base = nullptr;
 
+  // peer-memory exchange: round epoch (restarts with fresh peer buffers)
+  const void* p2p_buf = nullptr;
+  uint64_t p2p_epoch = 0;
+
   GreedyDev gr;                    // greedy assignment scratch (per n, in vec_bufs)
   int32_t gr_n = 0;
 
@@ -1131,9 +1135,27 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   const bool multi = dist && dist->world > 1;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world))
     return fail(ctx, LSAPGPU_ERR_INVALID, "invalid rank / world");
-  if (multi && (!dist->allgather || !dist->send_dev || !dist->recv_dev))
+  const bool p2p = multi && dist->peer_recv && dist->peer_flags;
+  if (multi && !p2p && (!dist->allgather || !dist->send_dev || !dist->recv_dev))
     return fail(ctx, LSAPGPU_ERR_INVALID, "multi-GPU solve needs an allgather callback and exchange buffers");
+  if (p2p && dist->world > kMaxPeers) return fail(ctx, LSAPGPU_ERR_INVALID, "peer transport: at most 8 ranks");
   const size_t xbytes = multi ? dist_exchange_bytes(n, dist->world) : 0;
+  PeerSet ps{};
+  if (p2p) {
+    for (int r = 0; r < dist->world; ++r) {
+      if (!dist->peer_recv[r] || !dist->peer_flags[r])
+        return fail(ctx, LSAPGPU_ERR_INVALID, "peer transport: missing peer buffer");
+      ps.recv[r] = static_cast<unsigned char*>(dist->peer_recv[r]);
+      ps.flags[r] = dist->peer_flags[r];
+    }
+    ps.world = dist->world;
+    ps.rank = dist->rank;
+    ps.bytes_per_rank = xbytes;
+    if (ctx->p2p_buf != dist->peer_recv[dist->rank]) {  // fresh (zeroed) flags: epochs restart
+      ctx->p2p_buf = dist->peer_recv[dist->rank];
+      ctx->p2p_epoch = 0;
+    }
+  }
   // one distributed step: this rank's items -> scan -> pack -> allgather -> merge
   auto dist_round = [&](int full) -> int {
     CK(launch_dist_own_items(d, full, dist->rank, dist->world, ctx->stream));
@@ -1143,6 +1165,15 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     ds.emit_edges = 0;
     CK(launch_scan(ds, ctx->scan_plan, 0, ctx->stream));
     ++ctx->launches;
+    if (p2p) {  // pack + allgather in one kernel over peer memory
+      const uint64_t epoch = ++ctx->p2p_epoch;
+      CK(launch_dist_push(d, ps, epoch, ctx->stream));
+      ctx->launches += 2;
+      CK(launch_dist_merge(d, ps.recv[ps.rank] + static_cast<size_t>(epoch & 1) * dist->world * xbytes,
+                           dist->world, xbytes, ctx->stream));
+      ++ctx->launches;
+      return LSAPGPU_OK;
+    }
     CK(launch_dist_pack(d, dist->send_dev, ctx->stream));
     ++ctx->launches;
     if (dist->allgather(dist->user, dist->send_dev, dist->recv_dev, xbytes, ctx->stream) != 0)
@@ -1320,8 +1351,10 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       if (first_pass) f_start = value;
       Ctrl& C = *ctx->ctrl_host;
       if (C.error) {
+        const int code = C.error;
         C.error = 0;
         push_ctrl(ctx);
+        if (code == 2) return fail(ctx, LSAPGPU_ERR_CUDA, "peer exchange: a rank's records did not arrive (timeout)");
         return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
       }
       const int64_t cnt = C.log_count;
@@ -1570,4 +1603,42 @@ int lsapgpu_greedy_assignment(lsapgpu_ctx* ctx, int32_t* sigma_out, int64_t* rou
   CK(cudaStreamSynchronize(ctx->stream));
   if (rounds) *rounds = gc.rounds;
   return LSAPGPU_OK;
+}
+
+size_t lsapgpu_dist_p2p_bytes(int32_t n, int32_t world) {
+  return 2 * static_cast<size_t>(world) * dist_exchange_bytes(n, world);  // double-buffered by epoch parity
+}
+
+int lsapgpu_dev_alloc(int device, size_t bytes, void** dev_ptr) {
+  if (!dev_ptr) return LSAPGPU_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(dev_ptr, bytes) != cudaSuccess ||
+      cudaMemset(*dev_ptr, 0, bytes) != cudaSuccess)
+    return LSAPGPU_ERR_CUDA;
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_dev_free(int device, void* dev_ptr) {
+  if (cudaSetDevice(device) != cudaSuccess || cudaFree(dev_ptr) != cudaSuccess) return LSAPGPU_ERR_CUDA;
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_ipc_handle(const void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return LSAPGPU_ERR_INVALID;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)) != cudaSuccess) return LSAPGPU_ERR_CUDA;
+  static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+  std::memcpy(handle64, &h, sizeof(h));
+  return LSAPGPU_OK;
+}
+
+int lsapgpu_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return LSAPGPU_ERR_INVALID;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? LSAPGPU_OK
+                                                                                         : LSAPGPU_ERR_CUDA;
+}
+
+int lsapgpu_ipc_close(void* dev_ptr) {
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? LSAPGPU_OK : LSAPGPU_ERR_CUDA;
 }

@@ -138,6 +138,15 @@ cudaError_t launch_dist_own_items(const DevState& d, int full, int32_t rank, int
 cudaError_t launch_dist_pack(const DevState& d, void* send, cudaStream_t st);
 cudaError_t launch_dist_merge(const DevState& d, const void* recv, int32_t world, size_t bytes_per_rank,
                               cudaStream_t st);
+constexpr int kMaxPeers = 8;
+struct PeerSet {  // receive buffers / flag arrays of every rank, mapped in this process
+  unsigned char* recv[kMaxPeers];
+  uint64_t* flags[kMaxPeers];
+  int32_t world, rank;
+  size_t bytes_per_rank;
+};
+// push this rank's records into every replica (buffer epoch & 1) and wait for all ranks'
+cudaError_t launch_dist_push(const DevState& d, const PeerSet& ps, uint64_t epoch, cudaStream_t st);
 
 // commit.cu
 enum CommitMode : int { kCommitSolve = 0, kCommitCheckOnly = 1, kCommitApplyOnly = 2 };

@@ -4,6 +4,11 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# Multi-rank tests run several ranks as threads on ONE device; with the
+# default 8 hardware work queues their streams can share a queue, and a rank
+# spinning on a peer flag (the peer transport) would then block the peer's
+# kernel behind it.  (One process per GPU in production never shares.)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

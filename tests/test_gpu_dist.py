@@ -11,10 +11,10 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def solve_ranks(a, cfg, world):
+def solve_ranks(a, cfg, world, peer=False):
     import paper_1106_5694_b200 as g
-    from paper_1106_5694_b200.dist import ThreadExchange
-    ex = ThreadExchange.group(world)
+    from paper_1106_5694_b200.dist import ThreadExchange, ThreadPeerExchange
+    ex = (ThreadPeerExchange if peer else ThreadExchange).group(world)
     out, errs = [None] * world, []
 
     def run(r):
@@ -32,6 +32,9 @@ def solve_ranks(a, cfg, world):
         t.start()
     for t in th:
         t.join(600)
+    if peer:
+        for e in ex:
+            e.free()
     if errs:
         raise errs[0]
     return out, ex
@@ -109,3 +112,85 @@ def test_multi_rank_greedy_start(oracle, gpu_ctx, world):
         assert np.array_equal(rep.assignment.sigma, ref.assignment.sigma)
         assert rep.assignment.value == ref.assignment.value
         assert rep.objective_trace == ref.objective_trace
+
+
+@pytest.mark.parametrize("kind,n,world,policy", [
+    ("int", 1000, 2, "touched_and_conflicted"), ("geom", 500, 3, "touched_only"),
+    ("f32", 2000, 4, "touched_and_conflicted"), ("p2p", 1500, 8, "touched_and_conflicted"),
+    ("int", 7, 4, "touched_and_conflicted")])
+def test_peer_transport_equals_single_gpu(oracle, gpu_ctx, kind, n, world, policy):
+    """The peer-memory transport (records pushed into every replica by the
+    pack kernel, epoch flags, no allgather call) with ranks as threads on one
+    device: bit-identical to the single-GPU solve, repeated solves included
+    (the epochs continue across solves)."""
+    import paper_1106_5694_b200 as g
+    from paper_1106_5694_b200.dist import ThreadPeerExchange
+    a = oracle.generate(kind, n, 5)
+    cfg = g.ParallelConfig(seed=3, reeval=policy)
+    gpu_ctx.set_matrix(a)
+    ref = gpu_ctx.solve(cfg)
+    ex = ThreadPeerExchange.group(world)
+    out, errs = [None] * world, []
+
+    def run(r):
+        try:
+            ctx = g.Context(0)
+            ctx.set_matrix(a)
+            out[r] = [ctx.solve(cfg, dist=ex[r]) for _ in range(2)]
+            ctx.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            ex[r].shared["barrier"].abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    for e in ex:
+        e.free()
+    if errs:
+        raise errs[0]
+    for reps in out:
+        for rep in reps:
+            assert np.array_equal(rep.assignment.sigma, ref.assignment.sigma)
+            assert rep.assignment.value == ref.assignment.value
+            assert rep.objective_trace == ref.objective_trace
+            assert rep.gpu["inner_iterations"] == ref.gpu["inner_iterations"]
+
+
+def test_peer_transport_two_processes_ipc(oracle, gpu_ctx, tmp_path):
+    """TorchPeerExchange across two real processes (CUDA IPC mappings of each
+    other's buffers, here on one device; NVLink peers on a multi-GPU node)."""
+    import os
+    import subprocess
+    import sys
+
+    import paper_1106_5694_b200 as g
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    a = oracle.generate("p2p", 1200, 11)
+    np.save(tmp_path / "a.npy", a)
+    script = tmp_path / "rank.py"
+    script.write_text(
+        "import os, sys, numpy as np, torch, torch.distributed as dist\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_1106_5694_b200 as g\n"
+        "from paper_1106_5694_b200.dist import TorchPeerExchange\n"
+        "dist.init_process_group('gloo')\n"
+        "torch.cuda.set_device(0)\n"
+        f"a = np.load({str(tmp_path / 'a.npy')!r})\n"
+        "ctx = g.Context(0); ctx.set_matrix(a)\n"
+        "ex = TorchPeerExchange()\n"
+        "rep = ctx.solve(g.ParallelConfig(seed=6), dist=ex)\n"
+        "rep = ctx.solve(g.ParallelConfig(seed=6), dist=ex)\n"
+        f"np.save(os.path.join({str(tmp_path)!r}, 'sigma%d.npy' % dist.get_rank()), rep.assignment.sigma)\n"
+        "dist.barrier(); ex.close(); ctx.close()\n"
+        "dist.destroy_process_group()\n")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29534", str(script)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    gpu_ctx.set_matrix(a)
+    ref = gpu_ctx.solve(g.ParallelConfig(seed=6))
+    for rank in range(2):
+        assert np.array_equal(np.load(tmp_path / f"sigma{rank}.npy"), ref.assignment.sigma)
