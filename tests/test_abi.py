@@ -17,7 +17,7 @@ GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
 def declared():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(lsapgpu_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(lsapgpu_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_library_exports_every_declared_symbol():
