@@ -109,6 +109,7 @@ struct Ctrl {
   uint32_t gbar_count, gbar_gen;
   uint32_t push_done;  // CTAs finished with the peer push of the current round
   uint32_t pad2_;
+  uint64_t p2p_epoch;  // peer transport: rounds pushed (flags carry it; graph-capturable)
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

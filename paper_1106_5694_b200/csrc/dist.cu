@@ -60,7 +60,8 @@ __global__ void pack_kernel(DevState st, unsigned char* send) {
 
 // Write every rank's records and append the active ones as proposals (Prop,
 // the layout the pair scan emits).
-__global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t world, size_t bytes_per_rank) {
+__device__ __forceinline__ void merge_body(const DevState& st, const unsigned char* recv, int32_t world,
+                                           size_t bytes_per_rank) {
   const int32_t n = st.n;
   const int P = st.ctrl->parity;
   for (int32_t r = 0; r < world; ++r) {
@@ -93,6 +94,10 @@ __global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t wor
   }
 }
 
+__global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t world, size_t bytes_per_rank) {
+  merge_body(st, recv, world, bytes_per_rank);
+}
+
 // ---- peer-memory exchange (NVLink / NVSwitch P2P) ------------------------
 // The pack step stores this rank's records straight into slot `rank` of every
 // replica's receive buffer (remote stores through peer mappings), fences at
@@ -101,8 +106,9 @@ __global__ void merge_kernel(DevState st, const unsigned char* recv, int32_t wor
 // buffers are double-buffered by epoch parity: a rank can only be one round
 // ahead of a peer (it waits for every peer's flag before its next push), so it
 // never overwrites the buffer that peer is still merging.
-__global__ void push_kernel(DevState st, PeerSet ps, uint64_t epoch) {
+__global__ void push_kernel(DevState st, PeerSet ps) {
   const int32_t count = st.ctrl->own_count;
+  const uint64_t epoch = st.ctrl->p2p_epoch + 1;  // advanced by the last CTA below
   const size_t slot = static_cast<size_t>(epoch & 1) * ps.world * ps.bytes_per_rank +
                       static_cast<size_t>(ps.rank) * ps.bytes_per_rank;
   if (blockIdx.x == 0 && threadIdx.x < ps.world)
@@ -121,25 +127,30 @@ __global__ void push_kernel(DevState st, PeerSet ps, uint64_t epoch) {
     if (r.agent < 0) r.agent = -2 - i;
     for (int32_t q = 0; q < ps.world; ++q) reinterpret_cast<Rec*>(ps.recv[q] + slot + 16)[k] = r;
   }
-  // the last CTA to finish raises the flags
+  // the last CTA to finish raises the flags and advances the epoch
   __threadfence_system();
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) last = atomicAdd(&st.ctrl->push_done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (last && threadIdx.x < ps.world) {
-    if (threadIdx.x == 0) st.ctrl->push_done = 0;
     __threadfence_system();
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ps.flags[threadIdx.x] + ps.rank), "l"(epoch)
                  : "memory");
+    __syncwarp((1u << ps.world) - 1u);
+    if (threadIdx.x == 0) {
+      st.ctrl->push_done = 0;
+      st.ctrl->p2p_epoch = epoch;
+    }
   }
 }
 
 // One warp waits until every rank's records of this epoch have landed (lane r
 // polls rank r's flag).  10 s without progress flags an error instead of
 // hanging the device.
-__global__ void peer_wait_kernel(PeerSet ps, uint64_t epoch, Ctrl* c) {
+__global__ void peer_wait_kernel(PeerSet ps, Ctrl* c) {
   const int r = threadIdx.x;
+  const uint64_t epoch = c->p2p_epoch;
   if (r < ps.world) {
     const uint64_t* f = ps.flags[ps.rank] + r;
     uint64_t t0;
@@ -160,13 +171,23 @@ __global__ void peer_wait_kernel(PeerSet ps, uint64_t epoch, Ctrl* c) {
   __syncwarp();
 }
 
+// merge_kernel on this rank's buffer of the current epoch
+__global__ void merge_p2p_kernel(DevState st, PeerSet ps) {
+  const unsigned char* recv =
+      ps.recv[ps.rank] + static_cast<size_t>(st.ctrl->p2p_epoch & 1) * ps.world * ps.bytes_per_rank;
+  merge_body(st, recv, ps.world, ps.bytes_per_rank);
+}
+
 }  // namespace
 
-cudaError_t launch_dist_push(const DevState& d, const PeerSet& ps, uint64_t epoch, cudaStream_t st) {
-  push_kernel<<<148, 256, 0, st>>>(d, ps, epoch);
+cudaError_t launch_dist_push(const DevState& d, const PeerSet& ps, cudaStream_t st) {
+  push_kernel<<<148, 256, 0, st>>>(d, ps);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  peer_wait_kernel<<<1, 32, 0, st>>>(ps, epoch, d.ctrl);
+  peer_wait_kernel<<<1, 32, 0, st>>>(ps, d.ctrl);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  merge_p2p_kernel<<<148, 256, 0, st>>>(d, ps);
   return cudaGetLastError();
 }
 

@@ -202,9 +202,12 @@ struct lsapgpu_ctx {
   uint64_t perm_seed = 0;
   Ctrl* ctrl_base = nullptr;
 
-  // peer-memory exchange: round epoch (restarts with fresh peer buffers)
-  const void* p2p_buf = nullptr;
-  uint64_t p2p_epoch = 0;
+  // multi-GPU inner-loop graph of the peer transport (commit, apply, own
+  // items, scan, push / wait / merge), cached like the single-GPU one
+  cudaGraphExec_t dist_exec = nullptr;
+  cudaGraph_t dist_graph = nullptr;
+  DevState dist_state;
+  PeerSet dist_ps;
 
   GreedyDev gr;                    // greedy assignment scratch (per n, in vec_bufs)
   int32_t gr_n = 0;
@@ -628,6 +631,43 @@ int build_graph(lsapgpu_ctx* ctx) {
   return LSAPGPU_OK;
 }
 
+// Inner-loop graph of the multi-GPU peer transport: no host step inside a
+// batch, so the whole {commit, apply, own items, scan, push, wait, merge}
+// loop is one conditional WHILE node, like the single-GPU graph.
+int build_dist_graph(lsapgpu_ctx* ctx, const PeerSet& ps) {
+  if (ctx->dist_exec) cudaGraphExecDestroy(ctx->dist_exec);
+  if (ctx->dist_graph) cudaGraphDestroy(ctx->dist_graph);
+  ctx->dist_exec = nullptr;
+  ctx->dist_graph = nullptr;
+  CK(cudaGraphCreate(&ctx->dist_graph, 0));
+  cudaGraphConditionalHandle cond;
+  CK(cudaGraphConditionalHandleCreate(&cond, ctx->dist_graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = cond;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, ctx->dist_graph, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  const DevState& d = ctx->d;
+  cudaError_t e = launch_commit(d, ctx->commit_plan, kCommitSolve, cond, 1, ctx->stream);
+  if (e == cudaSuccess) e = launch_dist_own_items(d, 0, ps.rank, ps.world, ctx->stream);
+  DevState ds = d;
+  ds.use_own = 1;
+  ds.emit_edges = 0;
+  if (e == cudaSuccess) e = launch_scan(ds, ctx->scan_plan, 0, ctx->stream);
+  if (e == cudaSuccess) e = launch_dist_push(d, ps, ctx->stream);
+  cudaGraph_t captured = body;
+  CK(cudaStreamEndCapture(ctx->stream, &captured));
+  CK(e);
+  CK(cudaGraphInstantiate(&ctx->dist_exec, ctx->dist_graph, 0));
+  ctx->dist_state = d;
+  ctx->dist_ps = ps;
+  return LSAPGPU_OK;
+}
+
 int run_scan(lsapgpu_ctx* ctx, int full) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(launch_scan(ctx->d, ctx->scan_plan, full, ctx->stream));
@@ -743,6 +783,8 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graph(ctx);
+  if (ctx->dist_exec) cudaGraphExecDestroy(ctx->dist_exec);
+  if (ctx->dist_graph) cudaGraphDestroy(ctx->dist_graph);
   free_vectors(ctx);
   if (ctx->mat.p) cudaFree(ctx->mat.p);
   if (ctx->ctrl_dev) cudaFree(ctx->ctrl_dev);
@@ -1136,6 +1178,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world))
     return fail(ctx, LSAPGPU_ERR_INVALID, "invalid rank / world");
   const bool p2p = multi && dist->peer_recv && dist->peer_flags;
+  const bool dist_graph = p2p && params && params->use_graph;  // the peer transport loop runs as a graph
   if (multi && !p2p && (!dist->allgather || !dist->send_dev || !dist->recv_dev))
     return fail(ctx, LSAPGPU_ERR_INVALID, "multi-GPU solve needs an allgather callback and exchange buffers");
   if (p2p && dist->world > kMaxPeers) return fail(ctx, LSAPGPU_ERR_INVALID, "peer transport: at most 8 ranks");
@@ -1151,10 +1194,14 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     ps.world = dist->world;
     ps.rank = dist->rank;
     ps.bytes_per_rank = xbytes;
-    if (ctx->p2p_buf != dist->peer_recv[dist->rank]) {  // fresh (zeroed) flags: epochs restart
-      ctx->p2p_buf = dist->peer_recv[dist->rank];
-      ctx->p2p_epoch = 0;
-    }
+    // the round epoch continues from this rank's own flag (every rank's last
+    // push; all ranks run the same sequence of solves on these buffers)
+    uint64_t e = 0;
+    CK(cudaMemcpyAsync(&e, dist->peer_flags[dist->rank] + dist->rank, sizeof(e), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpyAsync(&ctx->ctrl_dev->p2p_epoch, &e, sizeof(e), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
   }
   // one distributed step: this rank's items -> scan -> pack -> allgather -> merge
   auto dist_round = [&](int full) -> int {
@@ -1165,13 +1212,9 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     ds.emit_edges = 0;
     CK(launch_scan(ds, ctx->scan_plan, 0, ctx->stream));
     ++ctx->launches;
-    if (p2p) {  // pack + allgather in one kernel over peer memory
-      const uint64_t epoch = ++ctx->p2p_epoch;
-      CK(launch_dist_push(d, ps, epoch, ctx->stream));
-      ctx->launches += 2;
-      CK(launch_dist_merge(d, ps.recv[ps.rank] + static_cast<size_t>(epoch & 1) * dist->world * xbytes,
-                           dist->world, xbytes, ctx->stream));
-      ++ctx->launches;
+    if (p2p) {  // pack + allgather in one kernel over peer memory, then wait + merge
+      CK(launch_dist_push(d, ps, ctx->stream));
+      ctx->launches += 3;
       return LSAPGPU_OK;
     }
     CK(launch_dist_pack(d, dist->send_dev, ctx->stream));
@@ -1269,6 +1312,11 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       rc = build_graph(ctx);
       if (rc) return rc;
     }
+    if (dist_graph && (!ctx->dist_exec || std::memcmp(&ctx->dist_state, &d, sizeof(DevState)) != 0 ||
+                       std::memcmp(&ctx->dist_ps, &ps, sizeof(PeerSet)) != 0)) {
+      rc = build_dist_graph(ctx, ps);
+      if (rc) return rc;
+    }
   }
   ctx->scan_ms = ctx->full_ms = ctx->commit_ms = 0.0;
   ctx->scan_launches = ctx->full_launches = ctx->commit_launches = 0;
@@ -1298,7 +1346,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     S.agent_scans += n;
     S.job_scans += n;
     for (;;) {  // inner loop; repeats only to drain a full delta log
-      if (multi) {
+      if (multi && !dist_graph) {
         for (;;) {
           CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
           ctx->launches += ctx->commit_plan.launches();  // conflict check (+ apply)
@@ -1311,7 +1359,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
           ++launches;
         }
       } else if (P.use_graph) {
-        CK(cudaGraphLaunch(ctx->exec, ctx->stream));
+        CK(cudaGraphLaunch(dist_graph ? ctx->dist_exec : ctx->exec, ctx->stream));
         ++graph_launches;
         // control block and the first kLogPin log entries with one sync
         CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1438,13 +1486,16 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.job_scans += C.job_scans - base.job_scans;
   S.lfmm_rounds = C.lfmm_rounds - base.lfmm_rounds;
   S.switches_applied = switches;
-  const bool graphed = P.use_graph && !multi;
+  const bool graphed = P.use_graph && (!multi || dist_graph);
   S.scan_launches = graphed ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
   // every body pass of the graph is a commit (conflict check + apply) and a
   // scan launch; the last pass per graph launch finds no active record and
   // exits early
-  if (graphed)
-    ctx->launches += (1 + (d.fuse_apply ? 1 : ctx->commit_plan.launches())) * (S.inner_iterations + graph_launches);
+  if (graphed) {
+    const int per_pass = (d.fuse_apply ? 1 : ctx->commit_plan.launches()) +
+                         (dist_graph ? 2 /* own items */ + 1 /* scan */ + 3 /* push, wait, merge */ : 1);
+    ctx->launches += per_pass * (S.inner_iterations + graph_launches);
+  }
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;
 

@@ -145,8 +145,9 @@ struct PeerSet {  // receive buffers / flag arrays of every rank, mapped in this
   int32_t world, rank;
   size_t bytes_per_rank;
 };
-// push this rank's records into every replica (buffer epoch & 1) and wait for all ranks'
-cudaError_t launch_dist_push(const DevState& d, const PeerSet& ps, uint64_t epoch, cudaStream_t st);
+// push this rank's records into every replica (epoch = ++ctrl->p2p_epoch, buffer
+// epoch & 1), wait for every rank's flag, merge: the whole exchange, graph-capturable
+cudaError_t launch_dist_push(const DevState& d, const PeerSet& ps, cudaStream_t st);
 
 // commit.cu
 enum CommitMode : int { kCommitSolve = 0, kCommitCheckOnly = 1, kCommitApplyOnly = 2 };

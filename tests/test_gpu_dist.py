@@ -114,19 +114,23 @@ def test_multi_rank_greedy_start(oracle, gpu_ctx, world):
         assert rep.objective_trace == ref.objective_trace
 
 
-@pytest.mark.parametrize("kind,n,world,policy", [
-    ("int", 1000, 2, "touched_and_conflicted"), ("geom", 500, 3, "touched_only"),
-    ("f32", 2000, 4, "touched_and_conflicted"), ("p2p", 1500, 8, "touched_and_conflicted"),
-    ("int", 7, 4, "touched_and_conflicted")])
-def test_peer_transport_equals_single_gpu(oracle, gpu_ctx, kind, n, world, policy):
+@pytest.mark.parametrize("kind,n,world,policy,graph", [
+    ("int", 1000, 2, "touched_and_conflicted", True), ("geom", 500, 3, "touched_only", True),
+    ("f32", 2000, 4, "touched_and_conflicted", True), ("int", 7, 4, "touched_and_conflicted", True),
+    ("int", 1000, 2, "touched_and_conflicted", False), ("p2p", 1500, 8, "touched_and_conflicted", False)])
+def test_peer_transport_equals_single_gpu(oracle, gpu_ctx, kind, n, world, policy, graph):
     """The peer-memory transport (records pushed into every replica by the
     pack kernel, epoch flags, no allgather call) with ranks as threads on one
     device: bit-identical to the single-GPU solve, repeated solves included
-    (the epochs continue across solves)."""
+    (the epochs continue across solves).  Graph mode (the whole batch loop in
+    one graph launch per rank) is emulated with at most 4 ranks sharing the
+    device: more graphs spinning on peer flags on ONE GPU can starve each
+    other's device-side launches (with one process per GPU nothing is shared);
+    8 ranks run host-stepped."""
     import paper_1106_5694_b200 as g
     from paper_1106_5694_b200.dist import ThreadPeerExchange
     a = oracle.generate(kind, n, 5)
-    cfg = g.ParallelConfig(seed=3, reeval=policy)
+    cfg = g.ParallelConfig(seed=3, reeval=policy, use_graph=graph)
     gpu_ctx.set_matrix(a)
     ref = gpu_ctx.solve(cfg)
     ex = ThreadPeerExchange.group(world)
