@@ -1446,10 +1446,12 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       hmark("log replayed");
       const bool drained = C.drain;
       if (C.expired) expired = true;
+      if (!drained || expired) break;
+      // the log filled up mid-pass: empty it and continue the inner loop (a
+      // new pass's begin_pass resets it otherwise)
       begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);
       ++ctx->launches;  // log_count = 0, drain = 0
       CK(cudaGetLastError());
-      if (!drained || expired) break;
     }
     if (expired) break;
     if (P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns) {
@@ -1461,8 +1463,11 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   }
 
   if ((rc = ensure_init())) return rc;  // (a solve cut before its first pass)
-  // final counters, sigma / tau and the ordered objective with ONE sync
-  CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  // final counters, sigma / tau and the ordered objective with ONE sync (in
+  // graph mode the control block came with the last graph's read-back and no
+  // kernel since changed the counters)
+  const bool ctrl_current = P.use_graph && (!multi || dist_graph) && S.outer_iterations > 0 && !expired;
+  if (!ctrl_current) CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
   rc = enqueue_objective(ctx, true);  // snapshot_assignment (solver_state.hpp:141-148) + sigma / tau
   if (rc) return rc;
   hmark("final enqueued");
