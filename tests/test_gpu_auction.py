@@ -157,3 +157,14 @@ def test_auction_large_n_global_prices(oracle, gpu_ctx):
     want = oracle.auction_solve(a, epsilon=4.0)
     assert (rep.assignment.sigma == want.sigma).all()
     assert rep.outer_iterations == want.rounds and rep.switches_applied == want.switches
+
+
+def test_auction_randomised_sweep():
+    """tools/fuzz_auction.py: 150 random auction configurations vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_auction.py"), "150", "9"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

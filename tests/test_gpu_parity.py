@@ -456,3 +456,14 @@ def test_dgs_key_mode_boundary(oracle, gpu_ctx, n):
     want = oracle.dgs_parallel(a, seed=1, trace=False)
     assert np.array_equal(rep.assignment.sigma, want.sigma)
     assert rep.assignment.value == want.value and rep.switches_applied == want.switches_applied
+
+
+def test_randomised_parity_sweep():
+    """tools/fuzz_parity.py: 150 random configurations (kind, n, seeds,
+    policy, eps, graph / stepped, random / greedy start) vs the oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "150", "3"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
