@@ -162,11 +162,15 @@ __global__ void __launch_bounds__(256) commit_apply_kernel(DevState st) {
 }  // namespace
 
 cudaError_t launch_commit_apply(const DevState& d, cudaStream_t st) {
+  static const unsigned ctas = [] {
+    const char* e = std::getenv("LSAPGPU_APPLY_CTAS");
+    return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 64u;
+  }();
   switch (d.storage) {
-    case kI16: return launch_pdl(commit_apply_kernel<int16_t>, dim3(64), dim3(256), 0, st, d.pdl, d);
-    case kI32: return launch_pdl(commit_apply_kernel<int32_t>, dim3(64), dim3(256), 0, st, d.pdl, d);
-    case kF32: return launch_pdl(commit_apply_kernel<float>, dim3(64), dim3(256), 0, st, d.pdl, d);
-    case kF64: return launch_pdl(commit_apply_kernel<double>, dim3(64), dim3(256), 0, st, d.pdl, d);
+    case kI16: return launch_pdl(commit_apply_kernel<int16_t>, dim3(ctas), dim3(256), 0, st, d.pdl, d);
+    case kI32: return launch_pdl(commit_apply_kernel<int32_t>, dim3(ctas), dim3(256), 0, st, d.pdl, d);
+    case kF32: return launch_pdl(commit_apply_kernel<float>, dim3(ctas), dim3(256), 0, st, d.pdl, d);
+    case kF64: return launch_pdl(commit_apply_kernel<double>, dim3(ctas), dim3(256), 0, st, d.pdl, d);
     default: return cudaErrorInvalidValue;
   }
 }
