@@ -182,8 +182,11 @@ CommitPlan plan_commit(const DevState& d) {
   p.cluster_smem = budget;
   p.cluster = commit_cluster_size(d, budget);
   if (const char* s = std::getenv("LSAPGPU_COMMIT_CS")) p.cluster = std::atoi(s) == 8 ? 8 : p.cluster;
-  const size_t kslice = ((static_cast<size_t>(d.n) + p.cluster - 1) / p.cluster * 4 + 15) / 16 * 16;
-  const size_t cap = budget > 2 * kslice + 64 ? (budget - 2 * kslice - 64) / 45 : 0;
+  p.wide_keys = d.n >= (1 << 17) ? 1 : 0;  // slots 0..2n-1 no longer fit the 18-bit field
+  if (const char* s = std::getenv("LSAPGPU_LFMM64")) p.wide_keys = p.wide_keys || std::atoi(s) != 0;
+  const size_t slice = (static_cast<size_t>(d.n) + p.cluster - 1) / p.cluster;
+  const size_t kslice = 2 * ((slice * 4 + 15) / 16 * 16);  // keys + flags
+  const size_t cap = budget > kslice + 64 ? (budget - kslice - 64) / 45 : 0;
   p.edge_cap = static_cast<int>(cap / 16 * 16);
   // split commit (commit_single.cuh): per-agent keys + rejected-job bitmap,
   // 13 B per proposal, in one CTA's shared memory

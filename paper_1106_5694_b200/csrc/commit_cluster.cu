@@ -40,9 +40,7 @@ namespace lsapgpu {
 namespace {
 
 constexpr uint8_t kEdgeCommitted = 4;
-constexpr uint32_t kMatched = 0xFFFFFFFFu;
 constexpr uint32_t kKeyShift = 18;  // priorities (slots) < 2^18
-constexpr uint32_t kRoundLimit = (1u << 14) - 2;
 constexpr int kNT = 1024;
 constexpr uint32_t kTouched = 1u, kQueued = 2u, kJobRejected = 4u;
 constexpr int32_t kNoEmit = -1;
@@ -52,6 +50,28 @@ constexpr int32_t kSingleLoad = 2048;  // proposals rank 0 of the split commit l
 __device__ __forceinline__ uint32_t make_key(uint32_t round, int32_t slot) {
   return (round << kKeyShift) | (0x3FFFFu - static_cast<uint32_t>(slot));
 }
+
+// LFMM vertex keys (32 bit).  Narrow (n < 2^17): {14-bit round, 18-bit
+// inverted slot}, so keys of earlier rounds lose without clearing.  Wide (any
+// larger n; the reference has no size limit): the inverted slot alone, and
+// every CTA clears its unmatched keys before each round (one more cluster
+// barrier per round).  64-bit keys would need a 64-bit atomic max on
+// distributed shared memory, which the hardware emulates with a CAS loop on
+// the CTA's OWN shared memory (wrong for a peer's slice).
+template <bool kWide>
+struct LfmmKey;
+template <>
+struct LfmmKey<false> {
+  static constexpr uint32_t kMatched = 0xFFFFFFFFu;
+  static constexpr uint32_t kRoundLimit = (1u << 14) - 2;
+  __device__ static uint32_t make(uint32_t round, int32_t slot) { return make_key(round, slot); }
+};
+template <>
+struct LfmmKey<true> {
+  static constexpr uint32_t kMatched = 0xFFFFFFFFu;
+  static constexpr uint32_t kRoundLimit = 1;  // R >= 1 always: clear before every round
+  __device__ static uint32_t make(uint32_t, int32_t slot) { return 0xFFFFFFFEu - static_cast<uint32_t>(slot); }
+};
 
 __device__ __forceinline__ void block_add(int v, int* s) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
@@ -75,10 +95,12 @@ struct EdgeArrays {
   double *del, *acur_a, *acur_d;
 };
 
-template <class E, int CS>
+template <class E, int CS, bool kWide>
 __global__ void __launch_bounds__(kNT, 1)
     commit_cluster_kernel(DevState st, int mode, cudaGraphConditionalHandle cond, int use_cond,
                           int edge_cap, int cta_cap, int var, int fused) {
+  using KK = LfmmKey<kWide>;
+  using K = uint32_t;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int tid = threadIdx.x;
@@ -86,7 +108,7 @@ __global__ void __launch_bounds__(kNT, 1)
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CommitScratch sc;
-  __shared__ uint32_t* kbase[CS];
+  __shared__ K* kbase[CS];
   __shared__ uint32_t* fbase[CS];
 
   Ctrl* C = st.ctrl;
@@ -148,8 +170,9 @@ __global__ void __launch_bounds__(kNT, 1)
 
   // ---- P1: vertex slices, proposal endpoints ----
   const int32_t kslice = (n + CS - 1) / CS;
-  const size_t kbytes = ((static_cast<size_t>(kslice) * 4 + 15) / 16) * 16;
-  uint32_t* mykeys = reinterpret_cast<uint32_t*>(smem);
+  const size_t kbytes = ((static_cast<size_t>(kslice) * sizeof(K) + 15) / 16) * 16;
+  const size_t fbytes = ((static_cast<size_t>(kslice) * 4 + 15) / 16) * 16;
+  K* mykeys = reinterpret_cast<K*>(smem);
   uint32_t* myflags = reinterpret_cast<uint32_t*>(smem + kbytes);
   if (tid < CS) {
     kbase[tid] = cluster.map_shared_rank(mykeys, tid);
@@ -160,7 +183,7 @@ __global__ void __launch_bounds__(kNT, 1)
     sc.nlog = sc.nconf = sc.nconf_j = 0;
   }
   for (int32_t x = tid; x < kslice; x += kNT) {
-    mykeys[x] = 0u;
+    mykeys[x] = 0;
     myflags[x] = 0u;
   }
   if (mode == kCommitSolve && st.policy == 0) {  // this CTA's slice of the rejected-job bitmap
@@ -172,7 +195,7 @@ __global__ void __launch_bounds__(kNT, 1)
   const int32_t cnt = max(0, min(m, e0 + per) - e0);
   EdgeArrays Ea;
   if (per <= edge_cap) {
-    unsigned char* q = smem + 2 * kbytes;
+    unsigned char* q = smem + kbytes + fbytes;
     Ea.del = reinterpret_cast<double*>(q);
     q += static_cast<size_t>(edge_cap) * 8;
     Ea.acur_a = reinterpret_cast<double*>(q);
@@ -240,9 +263,9 @@ __global__ void __launch_bounds__(kNT, 1)
   uint32_t R = 1;
   int rounds = 0;
   for (;;) {
-    if (R >= kRoundLimit) {
+    if (R >= KK::kRoundLimit) {
       for (int32_t x = tid; x < kslice; x += kNT)
-        if (mykeys[x] != kMatched) mykeys[x] = 0u;
+        if (mykeys[x] != KK::kMatched) mykeys[x] = 0;
       R = 1;
       cluster.sync();
     }
@@ -250,16 +273,16 @@ __global__ void __launch_bounds__(kNT, 1)
     for (int32_t l = tid; l < cnt; l += kNT) {
       if (Ea.st[l] != kEdgeUndecided) continue;
       const int32_t u = Ea.u[l], v = Ea.v[l];
-      uint32_t* ku = kbase[u % CS] + u / CS;
-      uint32_t* kv = kbase[v % CS] + v / CS;
+      K* ku = kbase[u % CS] + u / CS;
+      K* kv = kbase[v % CS] + v / CS;
       const bool pre = rounds > 0 || (var & 1);  // nothing is matched in round 1
-      const uint32_t cu = pre ? *ku : 0u, cv = pre ? *kv : 0u;
-      if (cu == kMatched || cv == kMatched) {
+      const K cu = pre ? *ku : K(0), cv = pre ? *kv : K(0);
+      if (cu == KK::kMatched || cv == KK::kMatched) {
         Ea.st[l] = kEdgeRejected;
       } else {
         // keys only grow within a round: skip the (serialising, remote)
         // atomic when a higher priority is already posted
-        const uint32_t k = make_key(R, Ea.slot[l]);
+        const K k = KK::make(R, Ea.slot[l]);
         if (cu < k) atomicMax(ku, k);
         if (cv < k) atomicMax(kv, k);
         ++local;
@@ -280,13 +303,13 @@ __global__ void __launch_bounds__(kNT, 1)
     for (int32_t l = tid; l < cnt; l += kNT) {
       if (Ea.st[l] != kEdgeUndecided) continue;
       const int32_t u = Ea.u[l], v = Ea.v[l];
-      uint32_t* ku = kbase[u % CS] + u / CS;
-      uint32_t* kv = kbase[v % CS] + v / CS;
-      const uint32_t k = make_key(R, Ea.slot[l]);
+      K* ku = kbase[u % CS] + u / CS;
+      K* kv = kbase[v % CS] + v / CS;
+      const K k = KK::make(R, Ea.slot[l]);
       if (*ku == k && *kv == k) {
         Ea.st[l] = kEdgeAccepted;
-        *ku = kMatched;
-        *kv = kMatched;
+        *ku = KK::kMatched;
+        *kv = KK::kMatched;
       }
     }
     cluster.sync();
@@ -344,7 +367,7 @@ __global__ void __launch_bounds__(kNT, 1)
       bool q = false;
       if (l < cnt && Ea.st[l] == kEdgeRejected) {
         const int32_t p = Ea.u[l];  // the proposer (the record's owner)
-        q = kbase[p % CS][p / CS] != kMatched && !(atomicOr(fbase[p % CS] + p / CS, kQueued) & kQueued);
+        q = kbase[p % CS][p / CS] != KK::kMatched && !(atomicOr(fbase[p % CS] + p / CS, kQueued) & kQueued);
       }
       const unsigned qm = __ballot_sync(0xffffffffu, q);
       if (qm) {
@@ -524,7 +547,7 @@ __global__ void __launch_bounds__(kNT, 1)
 template <class E, int CS>
 cudaError_t launch_cs(const DevState& d, const CommitPlan& p, int mode, cudaGraphConditionalHandle cond,
                       int use_cond, cudaStream_t st) {
-  auto k = commit_cluster_kernel<E, CS>;
+  auto k = p.wide_keys ? commit_cluster_kernel<E, CS, true> : commit_cluster_kernel<E, CS, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(p.cluster_smem));
   if (e != cudaSuccess) return e;
@@ -569,7 +592,7 @@ cudaError_t launch_any(const DevState& d, const CommitPlan& p, int mode, cudaGra
 int commit_cluster_size(const DevState& d, size_t smem) {
   static int cached = 0;
   if (cached) return cached;
-  auto k = commit_cluster_kernel<int32_t, 16>;
+  auto k = commit_cluster_kernel<int32_t, 16, false>;
   int clusters = 0;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==

@@ -825,7 +825,7 @@ int lsapgpu_set_matrix_device(lsapgpu_ctx* ctx, const void* dev_data, int32_t n,
   CK(cudaSetDevice(ctx->device));
   if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
   if (dtype < 0 || dtype > 3) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown matrix dtype");
-  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  if (n >= (1 << 30)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 2^30 is not supported by this build");
   LayoutSource s;
   s.kind = 0;
   s.src = dev_data;
@@ -838,7 +838,7 @@ int lsapgpu_set_matrix(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dt
   CK(cudaSetDevice(ctx->device));
   if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
   if (dtype < 0 || dtype > 3) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown matrix dtype");
-  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  if (n >= (1 << 30)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 2^30 is not supported by this build");
   if (!data) return fail(ctx, LSAPGPU_ERR_INVALID, "null benefit matrix");
   return upload_host(ctx, data, n, dtype);
 }
@@ -848,7 +848,7 @@ int lsapgpu_generate(lsapgpu_ctx* ctx, int32_t kind, int32_t n, uint64_t seed, d
   CK(cudaSetDevice(ctx->device));
   if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "instance size must be >= 1, got " + std::to_string(n));
   if (kind < 1 || kind > 5) return fail(ctx, LSAPGPU_ERR_INVALID, "unknown generator kind");
-  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  if (n >= (1 << 30)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 2^30 is not supported by this build");
   if (kind == LSAPGPU_GEN_UNIFORM_INT && !(param >= 1.0))
     return fail(ctx, LSAPGPU_ERR_INVALID, "uniform int modulus must be >= 1");
   if (kind == LSAPGPU_GEN_GEOM && !(param > 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "geom: bound must be > 0");
@@ -1000,7 +1000,7 @@ int lsapgpu_check_conflicts(lsapgpu_ctx* ctx, int32_t n, const double* agent_del
   if (!ctx) return LSAPGPU_ERR_INVALID;
   CK(cudaSetDevice(ctx->device));
   if (n < 1) return fail(ctx, LSAPGPU_ERR_INVALID, "delta tables do not match assignment size");
-  if (n >= (1 << 17)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 131072 is not supported by this build");
+  if (n >= (1 << 30)) return fail(ctx, LSAPGPU_ERR_INVALID, "n >= 2^30 is not supported by this build");
   for (int32_t k = 0; k < n; ++k)
     if (agent_partner[k] >= n || job_partner[k] >= n || agent_partner[k] < -1 || job_partner[k] < -1)
       return fail(ctx, LSAPGPU_ERR_INVALID, "record partner out of range");

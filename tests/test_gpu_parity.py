@@ -116,6 +116,7 @@ def test_generators_match_oracle(oracle, gpu_ctx):
     {"LSAPGPU_COMMIT_FUSED_APPLY": "1"},                               # apply inside the cluster kernel
     {"LSAPGPU_COMMIT_FUSED_APPLY": "1", "LSAPGPU_COMMIT_SINGLE": "0"},
     {"LSAPGPU_FUSE_APPLY": "1"},                                       # apply inside the resident scan
+    {"LSAPGPU_LFMM64": "1", "LSAPGPU_COMMIT_SINGLE": "0"},            # 64-bit LFMM keys (n >= 2^17 path)
     {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
     {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
@@ -467,3 +468,20 @@ def test_randomised_parity_sweep():
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "150", "3"],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+
+def test_dgs_beyond_18bit_slots(gpu_ctx):
+    """n >= 2^17 (64-bit LFMM keys): a valid, deterministic assignment whose
+    value is the ordered objective (the oracle cannot hold the 137 GB fp64
+    instance here; the 64-bit key path itself is checked bit for bit at small
+    n through LSAPGPU_LFMM64=1 above)."""
+    n = (1 << 17) + 5
+    gpu_ctx.generate("int", n, 2, 1000.0)
+    cfg = _g().ParallelConfig(seed=1)
+    r1 = gpu_ctx.solve(cfg, trace=False)
+    r2 = gpu_ctx.solve(cfg, trace=False)
+    sig = r1.assignment.sigma
+    assert np.array_equal(np.sort(sig), np.arange(n, dtype=np.int32))
+    assert np.array_equal(sig, r2.assignment.sigma) and r1.assignment.value == r2.assignment.value
+    assert r1.switches_applied > 0 and r1.outer_iterations >= 2
