@@ -116,19 +116,24 @@ __global__ void __launch_bounds__(kNT, 1)
   const E* A = static_cast<const E*>(st.A);
   E* acur = static_cast<E*>(st.acur);
   const int64_t ld = st.ld;
+  // every control field in one round trip (independent loads: no dependent
+  // edge_count[parity] load, no short-circuit chain)
   const int P = C->parity;
-  const int32_t m = C->edge_count[P];
+  const int32_t ec0 = C->edge_count[0], ec1 = C->edge_count[1];
+  const int f_stop = C->expired | C->drain | C->error | C->inner_done;
+  const int64_t log_count = C->log_count;
+  const int32_t m = P ? ec1 : ec0;
   const Prop* edges = st.edges[P];
 
   if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, kTlCommit);
   // ---- P0: control ----
   if (mode == kCommitSolve) {
     int abort = 0;
-    if (C->expired || C->drain || C->error || C->inner_done)
+    if (f_stop)
       abort = 1;
     else if (m == 0)
       abort = 2;
-    else if (C->log_count + m > st.log_cap)
+    else if (log_count + m > st.log_cap)
       abort = 4;
     if (abort) {
       if (rank == 0 && tid == 0) {

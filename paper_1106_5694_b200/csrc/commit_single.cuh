@@ -71,7 +71,8 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
   Ctrl* C = st.ctrl;
   const int32_t n = st.n;
   const int P = C->parity;
-  const int32_t m = C->edge_count[P];
+  const int32_t ec0 = C->edge_count[0], ec1 = C->edge_count[1];  // (independent loads)
+  const int32_t m = P ? ec1 : ec0;
   const Prop* edges = st.edges[P];
   const int32_t iter = C->iter + 1;
 
