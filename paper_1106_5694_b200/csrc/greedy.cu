@@ -62,6 +62,8 @@ template <class E>
 __global__ void __launch_bounds__(kGT) greedy_kernel(DevState st, GreedyDev g) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint32_t s_free[];  // free-job bitmap of the round
+  __shared__ double s_pv[kGT / 32];
+  __shared__ int32_t s_pj[kGT / 32];
   const int32_t n = st.n;
   const int64_t ld = st.ld;
   const E* A = static_cast<const E*>(st.A);
@@ -93,25 +95,38 @@ __global__ void __launch_bounds__(kGT) greedy_kernel(DevState st, GreedyDev g) {
     const int32_t* list = cur ? g.list[1] : g.list[0];
     int32_t* next = cur ? g.list[0] : g.list[1];
 
-    // ---- claim: one warp per agent, best free job of its row ----
-    for (int32_t k = gwarp; k < cnt; k += nwarps) {
-      const int32_t i = __ldcg(list + k);
-      const uint4* rv = reinterpret_cast<const uint4*>(A + static_cast<int64_t>(i) * ld);
+    // ---- claim: G warps per agent (more when few agents remain), best free
+    // job of its row; the G partials merge through shared memory ----
+    constexpr int kWpc = kGT / 32;
+    int G = 1;
+    while (G < kWpc && static_cast<int64_t>(gridDim.x) * (kWpc / (2 * G)) >= cnt) G *= 2;
+    const int gpc = kWpc / G;
+    const int32_t ngroups = gridDim.x * gpc;
+    const int32_t grp = blockIdx.x * gpc + warp / G;
+    const int wig = warp % G;
+    for (int32_t base = 0; base < cnt; base += ngroups) {
+      const int32_t k = base + grp;
+      const bool valid = k < cnt;
       double bv = -__longlong_as_double(0x7FF0000000000000ll);
       int32_t bj = INT_MAX;
-      for (int32_t v = lane; v * VE < n; v += 32) {
-        const uint32_t fw = s_free[(v * VE) >> 5] >> ((v * VE) & 31);
-        if ((fw & ((1u << VE) - 1u)) == 0u) continue;  // no free job in this vector
-        const uint4 w = __ldg(rv + v);
-        const E* e = reinterpret_cast<const E*>(&w);
+      int32_t i = -1;
+      if (valid) {
+        i = __ldcg(list + k);
+        const uint4* rv = reinterpret_cast<const uint4*>(A + static_cast<int64_t>(i) * ld);
+        for (int32_t v = wig * 32 + lane; v * VE < n; v += G * 32) {
+          const uint32_t fw = s_free[(v * VE) >> 5] >> ((v * VE) & 31);
+          if ((fw & ((1u << VE) - 1u)) == 0u) continue;  // no free job in this vector
+          const uint4 w = __ldg(rv + v);
+          const E* e = reinterpret_cast<const E*>(&w);
 #pragma unroll
-        for (int q = 0; q < VE; ++q) {
-          const int32_t j = v * VE + q;
-          if (j < n && ((fw >> q) & 1u)) {
-            const double x = static_cast<double>(e[q]);
-            if (x > bv) {  // ascending j per lane: strict > keeps the first
-              bv = x;
-              bj = j;
+          for (int q = 0; q < VE; ++q) {
+            const int32_t j = v * VE + q;
+            if (j < n && ((fw >> q) & 1u)) {
+              const double x = static_cast<double>(e[q]);
+              if (x > bv) {  // ascending j per lane: strict > keeps the first
+                bv = x;
+                bj = j;
+              }
             }
           }
         }
@@ -125,7 +140,24 @@ __global__ void __launch_bounds__(kGT) greedy_kernel(DevState st, GreedyDev g) {
           bj = oj;
         }
       }
-      if (lane == 0) {
+      if (G > 1) {
+        if (lane == 0) {
+          s_pv[warp] = bv;
+          s_pj[warp] = bj;
+        }
+        __syncthreads();
+        if (valid && wig == 0 && lane == 0)
+          for (int w = 1; w < G; ++w) {
+            const double ov = s_pv[warp + w];
+            const int32_t oj = s_pj[warp + w];
+            if (ov > bv || (ov == bv && oj < bj)) {
+              bv = ov;
+              bj = oj;
+            }
+          }
+        __syncthreads();
+      }
+      if (valid && wig == 0 && lane == 0) {
         g.claim[i] = bj;
         post_claim(g.slot + 2 * static_cast<int64_t>(bj), bv, i);
       }
