@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kGT) greedy_kernel(DevState st, GreedyDev g) {
       if (valid) {
         i = __ldcg(list + k);
         const uint4* rv = reinterpret_cast<const uint4*>(A + static_cast<int64_t>(i) * ld);
+#pragma unroll 4
         for (int32_t v = wig * 32 + lane; v * VE < n; v += G * 32) {
           const uint32_t fw = s_free[(v * VE) >> 5] >> ((v * VE) & 31);
           if ((fw & ((1u << VE) - 1u)) == 0u) continue;  // no free job in this vector
