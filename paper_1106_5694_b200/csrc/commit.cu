@@ -183,7 +183,7 @@ CommitPlan plan_commit(const DevState& d) {
   p.cluster = commit_cluster_size(d, budget);
   if (const char* s = std::getenv("LSAPGPU_COMMIT_CS")) p.cluster = std::atoi(s) == 8 ? 8 : p.cluster;
   p.wide_keys = d.n >= (1 << 17) ? 1 : 0;  // slots 0..2n-1 no longer fit the 18-bit field
-  if (const char* s = std::getenv("LSAPGPU_LFMM64")) p.wide_keys = p.wide_keys || std::atoi(s) != 0;
+  if (const char* s = std::getenv("LSAPGPU_LFMM_WIDE")) p.wide_keys = p.wide_keys || std::atoi(s) != 0;
   const size_t slice = (static_cast<size_t>(d.n) + p.cluster - 1) / p.cluster;
   const size_t kslice = 2 * ((slice * 4 + 15) / 16 * 16);  // keys + flags
   const size_t cap = budget > kslice + 64 ? (budget - kslice - 64) / 45 : 0;

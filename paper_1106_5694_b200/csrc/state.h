@@ -160,7 +160,7 @@ struct CommitPlan {
   int edge_cap = 0;         // cluster kernel: proposals per CTA held in smem
   int cta_edge_cap = 0;     // single-CTA path taken when the proposals fit one CTA (0: never)
   int variant = 0;          // cluster kernel bit 0: read keys before the round-1 atomics
-  int wide_keys = 0;        // slot-only LFMM keys cleared every round (n >= 2^17, or LSAPGPU_LFMM64=1)
+  int wide_keys = 0;        // slot-only LFMM keys cleared every round (n >= 2^17, or LSAPGPU_LFMM_WIDE=1)
   int fused_apply = 0;      // split commit: the cluster kernel runs the apply itself (1, opt-in:
                             // measured 7 % slower at C3, 16 SMs of one GPC issue the scattered
                             // writes) or commit_apply_kernel follows it on 64 SMs (0)

@@ -116,7 +116,7 @@ def test_generators_match_oracle(oracle, gpu_ctx):
     {"LSAPGPU_COMMIT_FUSED_APPLY": "1"},                               # apply inside the cluster kernel
     {"LSAPGPU_COMMIT_FUSED_APPLY": "1", "LSAPGPU_COMMIT_SINGLE": "0"},
     {"LSAPGPU_FUSE_APPLY": "1"},                                       # apply inside the resident scan
-    {"LSAPGPU_LFMM64": "1", "LSAPGPU_COMMIT_SINGLE": "0"},            # 64-bit LFMM keys (n >= 2^17 path)
+    {"LSAPGPU_LFMM_WIDE": "1", "LSAPGPU_COMMIT_SINGLE": "0"},            # round-cleared LFMM keys (the n >= 2^17 path)
     {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
     {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
@@ -475,7 +475,7 @@ def test_dgs_beyond_18bit_slots(gpu_ctx):
     """n >= 2^17 (64-bit LFMM keys): a valid, deterministic assignment whose
     value is the ordered objective (the oracle cannot hold the 137 GB fp64
     instance here; the 64-bit key path itself is checked bit for bit at small
-    n through LSAPGPU_LFMM64=1 above)."""
+    n through LSAPGPU_LFMM_WIDE=1 above)."""
     n = (1 << 17) + 5
     gpu_ctx.generate("int", n, 2, 1000.0)
     cfg = _g().ParallelConfig(seed=1)
