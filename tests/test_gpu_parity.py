@@ -472,7 +472,7 @@ def test_randomised_parity_sweep():
 
 
 def test_dgs_beyond_18bit_slots(gpu_ctx):
-    """n >= 2^17 (64-bit LFMM keys): a valid, deterministic assignment whose
+    """n >= 2^17 (round-cleared LFMM keys): a valid, deterministic assignment whose
     value is the ordered objective (the oracle cannot hold the 137 GB fp64
     instance here; the 64-bit key path itself is checked bit for bit at small
     n through LSAPGPU_LFMM_WIDE=1 above)."""
