@@ -116,6 +116,7 @@ def test_generators_match_oracle(oracle, gpu_ctx):
     {"LSAPGPU_COMMIT_FUSED_APPLY": "1"},                               # apply inside the cluster kernel
     {"LSAPGPU_COMMIT_FUSED_APPLY": "1", "LSAPGPU_COMMIT_SINGLE": "0"},
     {"LSAPGPU_FUSE_APPLY": "1"},                                       # apply inside the resident scan
+    {"LSAPGPU_DEVICE_OUTER": "1"},                                     # whole solve as one graph (opt-in)
     {"LSAPGPU_LFMM_WIDE": "1", "LSAPGPU_COMMIT_SINGLE": "0"},            # round-cleared LFMM keys (the n >= 2^17 path)
     {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
     {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
