@@ -81,17 +81,20 @@ inline Context& context(int device) {
 }
 
 inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {}) {
-  inst.validate();
-  cfg.validate();
+  // Instance::validate (core.cpp:9-15) runs on the device during the upload
+  // (same checks, same messages, same precedence over cfg.validate()), so
+  // the O(n^2) host pass of the reference is not repeated here.
   Context& ctx = context(cfg.device);
   ctx.set_instance(inst);
+  cfg.validate();
   lsapgpu_params p{};
   p.seed = cfg.seed;
   p.eps = cfg.improvement_epsilon;
   p.reeval = cfg.reeval == ParallelConfig::Reeval::touched_only ? LSAPGPU_REEVAL_TOUCHED_ONLY
                                                                  : LSAPGPU_REEVAL_TOUCHED_AND_CONFLICTED;
   p.use_graph = cfg.use_graph ? 1 : 0;
-  p.deadline_ns = cfg.deadline ? static_cast<std::int64_t>(cfg.deadline->count()) : -1;
+  // Deadline::starting accepts any budget: zero or negative expires at once
+  p.deadline_ns = cfg.deadline ? std::max<std::int64_t>(0, static_cast<std::int64_t>(cfg.deadline->count())) : -1;
   p.init_sigma = nullptr;
   p.init_mode = cfg.greedy_init ? LSAPGPU_INIT_GREEDY : LSAPGPU_INIT_RANDOM;
   const std::int32_t n = inst.n;
@@ -99,12 +102,22 @@ inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {})
   rep.assignment.sigma.resize(n);
   rep.assignment.tau.resize(n);
   lsapgpu_stats st{};
-  const std::int64_t cap = 100000 + 4096;
+  std::int64_t cap = 100000 + 4096;
   std::vector<std::int64_t> ts(cap);
   std::vector<double> tv(cap);
   std::int64_t tl = 0;
   ctx.check(lsapgpu_solve(ctx.get(), &p, rep.assignment.sigma.data(), rep.assignment.tau.data(), &st,
                           ts.data(), tv.data(), cap, &tl));
+  if (tl > cap && !cfg.deadline) {
+    // the reference's trace keeps growing by one entry per outer pass past its
+    // 100000 cap (parallel.cpp:15-20,343-344): re-run with room for all of it
+    // (the solve is deterministic without a deadline)
+    cap = tl;
+    ts.assign(cap, 0);
+    tv.assign(cap, 0.0);
+    ctx.check(lsapgpu_solve(ctx.get(), &p, rep.assignment.sigma.data(), rep.assignment.tau.data(), &st,
+                            ts.data(), tv.data(), cap, &tl));
+  }
   rep.assignment.value = st.value;
   rep.outer_iterations = st.outer_iterations;
   rep.switches_applied = st.switches_applied;
@@ -118,11 +131,10 @@ inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {})
 
 inline void evaluate_all_parallel(const Instance& inst, const Assignment& asg, DeltaTables& tables,
                                   const GpuConfig& cfg = {}) {
-  inst.validate();
+  Context& ctx = context(cfg.device);
+  ctx.set_instance(inst);  // Instance::validate on the device
   cfg.validate();
   if (asg.size() != inst.n) throw Error("assignment does not match instance");
-  Context& ctx = context(cfg.device);
-  ctx.set_instance(inst);
   const std::int32_t n = inst.n;
   std::vector<double> ad(n), jd(n);
   std::vector<std::int32_t> ap(n), jp(n);
@@ -170,12 +182,11 @@ inline ConflictSets check_conflicts(const DeltaTables& tables, const Assignment&
 inline std::pair<Assignment, std::vector<AppliedExchange>> apply_parallel_switches(
     const Instance& inst, const Assignment& asg, const DeltaTables& tables, const ConflictSets& sets,
     const GpuConfig& cfg = {}) {
-  inst.validate();
+  Context& ctx = context(cfg.device);
+  ctx.set_instance(inst);  // Instance::validate on the device
   cfg.validate();
   const std::int32_t n = inst.n;
   if (asg.size() != n) throw Error("assignment does not match instance");
-  Context& ctx = context(cfg.device);
-  ctx.set_instance(inst);
   std::vector<double> ad(n), jd(n);
   std::vector<std::int32_t> ap(n), jp(n);
   std::vector<std::uint8_t> aa(n), ja(n);
@@ -209,16 +220,15 @@ inline std::pair<Assignment, std::vector<AppliedExchange>> apply_parallel_switch
 inline SolveReport auction_solve(const Instance& inst, const AuctionConfig& cfg = {},
                                  const std::function<void(const std::vector<double>&)>& on_round = {},
                                  int device = 0, std::int64_t round_cap = 4096) {
-  inst.validate();
-  cfg.validate();
   Context& ctx = context(device);
-  ctx.set_instance(inst);
+  ctx.set_instance(inst);  // Instance::validate on the device
+  cfg.validate();
   lsapgpu_auction_params p{};
   p.has_epsilon = cfg.epsilon ? 1 : 0;
   p.epsilon = cfg.epsilon ? *cfg.epsilon : 0.0;
   p.scaling = cfg.scaling ? 1 : 0;
   p.scale_factor = cfg.scale_factor;
-  p.deadline_ns = cfg.deadline ? static_cast<std::int64_t>(cfg.deadline->count()) : -1;
+  p.deadline_ns = cfg.deadline ? std::max<std::int64_t>(0, static_cast<std::int64_t>(cfg.deadline->count())) : -1;
   const std::int32_t n = inst.n;
   SolveReport rep;
   rep.assignment.sigma.resize(n);

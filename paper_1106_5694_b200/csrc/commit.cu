@@ -199,7 +199,6 @@ CommitPlan plan_commit(const DevState& d) {
     if (std::atoi(s) == 0) p.cta_edge_cap = 0;
   if (const char* s = std::getenv("LSAPGPU_COMMIT_SINGLE_MAX")) p.cta_edge_cap = std::min(p.cta_edge_cap, std::atoi(s));
   if (const char* s = std::getenv("LSAPGPU_COMMIT_VARIANT")) p.variant = std::atoi(s);
-  if (const char* s = std::getenv("LSAPGPU_COMMIT_FUSED_APPLY")) p.fused_apply = std::atoi(s) != 0;
   return p;
 }
 
@@ -207,7 +206,7 @@ cudaError_t launch_commit(const DevState& d, const CommitPlan& p, int mode,
                           cudaGraphConditionalHandle cond, int use_cond, cudaStream_t st) {
   if (mode == kCommitApplyOnly) return cudaErrorInvalidValue;  // launch_accepted_from_masks
   cudaError_t e = launch_commit_cluster(d, p, mode, cond, use_cond, st);
-  if (e != cudaSuccess || mode != kCommitSolve || p.fused_apply || d.fuse_apply) return e;
+  if (e != cudaSuccess || mode != kCommitSolve) return e;
   return launch_commit_apply(d, st);
 }
 

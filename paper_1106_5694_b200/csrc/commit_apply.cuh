@@ -1,8 +1,7 @@
 // commit_apply.cuh -- the scattered writes of one batch under the split
 // commit (select / apply / re-evaluation items, parallel.cpp:276-330), as a
-// device function run by every thread of the grid that calls it: the cluster
-// commit kernel after its conflict check (fused, the default) or the
-// stand-alone commit_apply_kernel (LSAPGPU_COMMIT_FUSED_APPLY=0).
+// device function run by every thread of commit_apply_kernel (commit.cu),
+// which follows the conflict check on 64 SMs.
 #pragma once
 
 #include "state.h"

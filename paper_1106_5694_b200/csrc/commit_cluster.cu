@@ -98,7 +98,7 @@ struct EdgeArrays {
 template <class E, int CS, bool kWide>
 __global__ void __launch_bounds__(kNT, 1)
     commit_cluster_kernel(DevState st, int mode, cudaGraphConditionalHandle cond, int use_cond,
-                          int edge_cap, int cta_cap, int var, int fused) {
+                          int edge_cap, int cta_cap, int var) {
   using KK = LfmmKey<kWide>;
   using K = uint32_t;
   cg::cluster_group cluster = cg::this_cluster();
@@ -163,11 +163,6 @@ __global__ void __launch_bounds__(kNT, 1)
       single::load_share(st, cta_cap, dst, min(m, rank * per), min(m, (rank + 1) * per));
       cluster.sync();
       if (rank == 0) single::commit_single(st, mode, cta_cap, smem, true, !(var & 2));
-    }
-    if (mode == kCommitSolve && fused) {  // the batch's scattered writes, cluster-wide
-      cluster.sync();
-      if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 15);
-      apply_batch<E>(st, static_cast<int64_t>(rank) * kNT + tid, static_cast<int64_t>(CS) * kNT);
     }
     return;
   }
@@ -407,13 +402,8 @@ __global__ void __launch_bounds__(kNT, 1)
       C->edge_count[P] = 0;
       C->lfmm_rounds += rounds;
       C->inner_iterations += 1;
-      if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
+      if (!st.dist_vote && C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
       tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
-    }
-    if (mode == kCommitSolve && fused) {
-      cluster.sync();  // batch counters written
-      if (rank == 0 && tid == 0) tl_mark(C, st.tl, st.tl_cap, 15);
-      apply_batch<E>(st, static_cast<int64_t>(rank) * kNT + tid, static_cast<int64_t>(CS) * kNT);
     }
     return;
   }
@@ -544,7 +534,7 @@ __global__ void __launch_bounds__(kNT, 1)
     C->lfmm_rounds += rounds;
     C->inner_iterations += 1;
     // anytime deadline, acted on by the next commit (solver_state.hpp:13-27)
-    if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
+    if (!st.dist_vote && C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
     tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
   }
 }
@@ -574,8 +564,7 @@ cudaError_t launch_cs(const DevState& d, const CommitPlan& p, int mode, cudaGrap
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = d.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap, p.variant,
-                            p.fused_apply);
+  return cudaLaunchKernelEx(&cfg, k, d, mode, cond, use_cond, p.edge_cap, p.cta_edge_cap, p.variant);
 }
 
 template <int CS>

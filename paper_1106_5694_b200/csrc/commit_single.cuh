@@ -220,7 +220,7 @@ __device__ __forceinline__ void commit_single(const DevState& st, int mode, int 
     C->lfmm_rounds += rounds;
     C->inner_iterations += 1;
     // anytime deadline, acted on by the next commit (solver_state.hpp:13-27)
-    if (C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
+    if (!st.dist_vote && C->deadline_gt != 0 && globaltimer() >= C->deadline_gt) C->expired = 1;
     tl_mark(C, st.tl, st.tl_cap, kTlCommitEnd);
   }
 }

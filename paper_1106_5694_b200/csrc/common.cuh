@@ -110,10 +110,6 @@ struct Ctrl {
   uint32_t push_done;  // CTAs finished with the peer push of the current round
   uint32_t pad2_;
   uint64_t p2p_epoch;  // peer transport: rounds pushed (flags carry it; graph-capturable)
-  // device-driven outer loop (integer storage): passes run and the log
-  // position at the end of each
-  int32_t outer_passes;
-  int32_t pass_end[16];
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

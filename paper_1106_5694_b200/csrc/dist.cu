@@ -6,7 +6,11 @@
 // then runs replicated: its result does not depend on proposal order, so all
 // ranks apply identical batches and sigma never needs a broadcast.
 //
-// Exchange buffer per rank: 16-byte header {count} + count x Rec (32 B).
+// Exchange buffer per rank: 16-byte header {count, deadline vote} + count x
+// Rec (32 B).  The vote is this rank's %globaltimer deadline test at push
+// time; the merge ORs every rank's vote into ctrl->expired, so the ranks agree
+// on expiry at the same batch (a rank stopping alone would leave its peers
+// waiting on a push that never comes).
 // Two transports: the caller's allgather (e.g. NCCL) between pack and merge,
 // or the peer-memory push below (pack + allgather in one kernel).
 #include "state.h"
@@ -36,10 +40,17 @@ __global__ void own_items_kernel(DevState st, int full, int32_t rank, int32_t wo
 
 __global__ void reset_own_kernel(Ctrl* c) { c->own_count = 0; }
 
+__device__ __forceinline__ long long deadline_vote(const Ctrl* c) {
+  return (c->deadline_gt != 0 && globaltimer() >= c->deadline_gt) ? 1 : 0;
+}
+
 __global__ void pack_kernel(DevState st, unsigned char* send) {
   const int32_t count = st.ctrl->own_count;
   Rec* out = reinterpret_cast<Rec*>(send + 16);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<long long*>(send) = count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    reinterpret_cast<long long*>(send)[0] = count;
+    reinterpret_cast<long long*>(send)[1] = deadline_vote(st.ctrl);
+  }
   for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
     const uint32_t w = st.items_own[k];
     const int32_t i = static_cast<int32_t>(w & kItemMask);
@@ -64,6 +75,12 @@ __device__ __forceinline__ void merge_body(const DevState& st, const unsigned ch
                                            size_t bytes_per_rank) {
   const int32_t n = st.n;
   const int P = st.ctrl->parity;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long vote = 0;
+    for (int32_t r = 0; r < world; ++r)
+      vote |= reinterpret_cast<const long long*>(recv + static_cast<size_t>(r) * bytes_per_rank)[1];
+    if (vote) st.ctrl->expired = 1;  // acted on by the next commit, on every rank alike
+  }
   for (int32_t r = 0; r < world; ++r) {
     const unsigned char* base = recv + static_cast<size_t>(r) * bytes_per_rank;
     const int32_t count = static_cast<int32_t>(*reinterpret_cast<const long long*>(base));
@@ -111,8 +128,10 @@ __global__ void push_kernel(DevState st, PeerSet ps) {
   const uint64_t epoch = st.ctrl->p2p_epoch + 1;  // advanced by the last CTA below
   const size_t slot = static_cast<size_t>(epoch & 1) * ps.world * ps.bytes_per_rank +
                       static_cast<size_t>(ps.rank) * ps.bytes_per_rank;
-  if (blockIdx.x == 0 && threadIdx.x < ps.world)
-    *reinterpret_cast<long long*>(ps.recv[threadIdx.x] + slot) = count;
+  if (blockIdx.x == 0 && threadIdx.x < ps.world) {
+    reinterpret_cast<long long*>(ps.recv[threadIdx.x] + slot)[0] = count;
+    reinterpret_cast<long long*>(ps.recv[threadIdx.x] + slot)[1] = deadline_vote(st.ctrl);
+  }
   for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
     const uint32_t w = st.items_own[k];
     const int32_t i = static_cast<int32_t>(w & kItemMask);

@@ -54,32 +54,6 @@ __global__ void set_deadline_kernel(Ctrl* c, int64_t remaining_ns) {
   c->deadline_gt = remaining_ns < 0 ? 0ull : globaltimer() + static_cast<uint64_t>(remaining_ns);
 }
 
-// Device-driven outer loop (integer storage: a pass with any switch changes
-// the value, so "another pass?" is decided on the device from the log; the
-// host replays every pass's log after ONE graph launch).
-constexpr int kMaxDevPasses = 16;
-__global__ void solve_begin_kernel(Ctrl* c) {
-  c->log_count = 0;
-  c->outer_passes = 0;
-  c->drain = 0;
-}
-__global__ void outer_begin_kernel(Ctrl* c, cudaGraphConditionalHandle inner) {
-  c->edge_count[0] = 0;  // begin_pass(1) without the log reset
-  c->edge_count[1] = 0;
-  c->inner_done = 0;
-  cudaGraphSetConditional(inner, 1);
-}
-__global__ void outer_end_kernel(Ctrl* c, cudaGraphConditionalHandle outer, int64_t log_cap) {
-  const int k = c->outer_passes;
-  const int64_t lc = c->log_count;
-  const int64_t prev = k ? c->pass_end[k - 1] : 0;
-  c->pass_end[k] = static_cast<int32_t>(lc);
-  c->outer_passes = k + 1;
-  if (c->deadline_gt != 0 && globaltimer() >= c->deadline_gt) c->expired = 1;  // pass-boundary deadline check
-  if (c->error || c->expired || c->drain || lc == prev || k + 1 >= kMaxDevPasses || lc > log_cap / 2)
-    cudaGraphSetConditional(outer, 0);
-}
-
 // Start of an outer pass (or of a resumed inner loop after a log drain).
 __global__ void begin_pass_kernel(Ctrl* c, int full) {
   if (full) {
@@ -231,12 +205,6 @@ struct lsapgpu_ctx {
   // multi-GPU inner-loop graph of the peer transport (commit, apply, own
   // items, scan, push / wait / merge), cached like the single-GPU one
   // device-driven outer loop graph (integer storage, single GPU)
-  cudaGraphExec_t outer_exec = nullptr;
-  cudaGraph_t outer_graph = nullptr;
-  DevState outer_state;
-  ScanPlan outer_scan;
-  CommitPlan outer_commit;
-  int64_t outer_log_hint = 1 << 16;  // log entries of the last device-driven solve
   cudaGraphExec_t dist_exec = nullptr;
   cudaGraph_t dist_graph = nullptr;
   DevState dist_state;
@@ -701,70 +669,6 @@ int build_dist_graph(lsapgpu_ctx* ctx, const PeerSet& ps) {
   return LSAPGPU_OK;
 }
 
-// Graph of a whole solve for integer storage: WHILE(more passes) { pass
-// prologue, full sweep, WHILE(active records) { commit, apply, scan },
-// outer_end }.  The host launches it once and replays the log afterwards.
-int build_outer_graph(lsapgpu_ctx* ctx) {
-  if (ctx->outer_exec) cudaGraphExecDestroy(ctx->outer_exec);
-  if (ctx->outer_graph) cudaGraphDestroy(ctx->outer_graph);
-  ctx->outer_exec = nullptr;
-  ctx->outer_graph = nullptr;
-  CK(cudaGraphCreate(&ctx->outer_graph, 0));
-  cudaGraphConditionalHandle h_outer, h_inner;
-  CK(cudaGraphConditionalHandleCreate(&h_outer, ctx->outer_graph, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams po = {};
-  po.type = cudaGraphNodeTypeConditional;
-  po.conditional.handle = h_outer;
-  po.conditional.type = cudaGraphCondTypeWhile;
-  po.conditional.size = 1;
-  cudaGraphNode_t wo;
-  CK(cudaGraphAddNode(&wo, ctx->outer_graph, nullptr, 0, &po));
-  cudaGraph_t body = po.conditional.phGraph_out[0];
-  CK(cudaGraphConditionalHandleCreate(&h_inner, body, 1, cudaGraphCondAssignDefault));
-  const DevState& d = ctx->d;
-  // pass prologue + full sweep
-  CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  outer_begin_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, h_inner);
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = launch_scan(d, ctx->scan_plan, 1, ctx->stream);
-  cudaStreamCaptureStatus cs;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t ndeps = 0;
-  cudaError_t e2 = cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, nullptr, &deps, &ndeps);
-  std::vector<cudaGraphNode_t> sink(deps, deps + ndeps);
-  cudaGraph_t cap = body;
-  CK(cudaStreamEndCapture(ctx->stream, &cap));
-  CK(e);
-  CK(e2);
-  // the inner batch loop
-  cudaGraphNodeParams pi = {};
-  pi.type = cudaGraphNodeTypeConditional;
-  pi.conditional.handle = h_inner;
-  pi.conditional.type = cudaGraphCondTypeWhile;
-  pi.conditional.size = 1;
-  cudaGraphNode_t wi;
-  CK(cudaGraphAddNode(&wi, body, sink.data(), sink.size(), &pi));
-  cudaGraph_t ibody = pi.conditional.phGraph_out[0];
-  CK(cudaStreamBeginCaptureToGraph(ctx->stream, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  e = launch_commit(d, ctx->commit_plan, kCommitSolve, h_inner, 1, ctx->stream);
-  if (e == cudaSuccess) e = launch_scan(d, ctx->scan_plan, 0, ctx->stream);
-  cap = ibody;
-  CK(cudaStreamEndCapture(ctx->stream, &cap));
-  CK(e);
-  // pass epilogue: record the pass, decide on the next one
-  CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, &wi, nullptr, 1, cudaStreamCaptureModeThreadLocal));
-  outer_end_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, h_outer, d.log_cap);
-  e = cudaGetLastError();
-  cap = body;
-  CK(cudaStreamEndCapture(ctx->stream, &cap));
-  CK(e);
-  CK(cudaGraphInstantiate(&ctx->outer_exec, ctx->outer_graph, 0));
-  ctx->outer_state = d;
-  ctx->outer_scan = ctx->scan_plan;
-  ctx->outer_commit = ctx->commit_plan;
-  return LSAPGPU_OK;
-}
-
 int run_scan(lsapgpu_ctx* ctx, int full) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(launch_scan(ctx->d, ctx->scan_plan, full, ctx->stream));
@@ -882,8 +786,6 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   drop_graph(ctx);
   if (ctx->dist_exec) cudaGraphExecDestroy(ctx->dist_exec);
   if (ctx->dist_graph) cudaGraphDestroy(ctx->dist_graph);
-  if (ctx->outer_exec) cudaGraphExecDestroy(ctx->outer_exec);
-  if (ctx->outer_graph) cudaGraphDestroy(ctx->outer_graph);
   free_vectors(ctx);
   if (ctx->mat.p) cudaFree(ctx->mat.p);
   if (ctx->ctrl_dev) cudaFree(ctx->ctrl_dev);
@@ -1293,12 +1195,17 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     ps.world = dist->world;
     ps.rank = dist->rank;
     ps.bytes_per_rank = xbytes;
-    // the round epoch continues from this rank's own flag (every rank's last
-    // push; all ranks run the same sequence of solves on these buffers)
-    uint64_t e = 0;
-    CK(cudaMemcpyAsync(&e, dist->peer_flags[dist->rank] + dist->rank, sizeof(e), cudaMemcpyDeviceToHost,
+    // the round epoch continues from the highest flag any rank has raised in
+    // this rank's buffer: every push raises its flag in every replica, so all
+    // ranks start from the same epoch, above anything already written -- also
+    // after a solve that one rank left early with an error (no stale buffer
+    // can then pass a wait)
+    uint64_t fl[kMaxPeers] = {};
+    CK(cudaMemcpyAsync(fl, dist->peer_flags[dist->rank], sizeof(uint64_t) * dist->world, cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    uint64_t e = 0;
+    for (int r = 0; r < dist->world; ++r) e = std::max(e, fl[r]);
     CK(cudaMemcpyAsync(&ctx->ctrl_dev->p2p_epoch, &e, sizeof(e), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
@@ -1388,18 +1295,13 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     if (host_timing) hmarks.emplace_back(what, elapsed_ns());
   };
   hmark("init+objective");
-  bool expired = P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns;
+  // multi-rank: only the budget 0 is decided here (identically on every rank);
+  // any other expiry is agreed at a record exchange (dist.cu)
+  bool expired = P.deadline_ns >= 0 && (multi ? P.deadline_ns == 0 : elapsed_ns() >= P.deadline_ns);
 
   d.eps = P.eps;
+  d.dist_vote = multi ? 1 : 0;
   d.policy = P.reeval;
-  // single GPU + resident scan: LSAPGPU_FUSE_APPLY=1 lets the scan run each
-  // batch's apply itself behind a grid barrier instead of commit_apply_kernel
-  // (opt-in: measured 5 % slower at C3 -- the barrier waits for the CTAs the
-  // commit cluster's SMs delay, where PDL overlaps the small apply kernel)
-  {
-    static const bool fuse_env = std::getenv("LSAPGPU_FUSE_APPLY") && std::atoi(std::getenv("LSAPGPU_FUSE_APPLY"));
-    d.fuse_apply = (!multi && ctx->scan_plan.resident && fuse_env) ? 1 : 0;
-  }
   if (!expired) {
     set_deadline_kernel<<<1, 1, 0, ctx->stream>>>(
         ctx->ctrl_dev, P.deadline_ns < 0 ? -1 : std::max<int64_t>(0, P.deadline_ns - elapsed_ns()));
@@ -1427,117 +1329,9 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   bool prefetched = false;  // ctrl + log prefix already read back with the graph's sync
   int64_t pin_len = 0;      // entries of that prefix
 
-  // Device-driven outer loop (opt-in, LSAPGPU_DEVICE_OUTER=1; integer storage,
-  // one GPU, graph mode): the whole solve is one graph launch with nested
-  // conditional WHILE nodes and the host replays each pass's log afterwards.
-  // Measured neutral (C3 +0.5 %, C1 -3 %): the host gap between the two
-  // passes it removes is about what the nested conditional costs.
-  bool dev_done = false, resume_inner = false;
-  double resume_f_start = 0.0;
-  int64_t dev_passes = 0;
-  {
-    static const bool dev_env = std::getenv("LSAPGPU_DEVICE_OUTER") && std::atoi(std::getenv("LSAPGPU_DEVICE_OUTER"));
-    const bool dev_outer = dev_env && P.use_graph && !multi && (d.storage == kI16 || d.storage == kI32) && !expired;
-    if (dev_outer) {
-      if (!ctx->outer_exec || std::memcmp(&ctx->outer_state, &d, sizeof(DevState)) != 0 ||
-          !(ctx->outer_scan == ctx->scan_plan) || !(ctx->outer_commit == ctx->commit_plan)) {
-        rc = build_outer_graph(ctx);
-        if (rc) return rc;
-      }
-      solve_begin_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev);
-      ++ctx->launches;
-      CK(cudaGetLastError());
-      CK(cudaGraphLaunch(ctx->outer_exec, ctx->stream));
-      const int64_t pl = std::min<int64_t>(std::min<int64_t>(lsapgpu_ctx::kLogPin, d.log_cap),
-                                           ctx->outer_log_hint + ctx->outer_log_hint / 4 + 1024);
-      CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cpy(ctx, ctx->log_pin, d.log, sizeof(LogEntry) * pl, cudaMemcpyDeviceToHost, ctx->stream));
-      hmark("outer graph launched");
-      CK(cudaStreamSynchronize(ctx->stream));
-      hmark("outer graph done");
-      if ((rc = ensure_init())) return rc;
-      Ctrl& C = *ctx->ctrl_host;
-      if (C.error) {
-        C.error = 0;
-        push_ctrl(ctx);
-        return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
-      }
-      const int passes = C.outer_passes;
-      dev_passes = passes;
-      S.outer_iterations = passes;
-      S.pair_items += static_cast<int64_t>(passes) * n;
-      S.agent_scans += static_cast<int64_t>(passes) * n;
-      S.job_scans += static_cast<int64_t>(passes) * n;
-      const int64_t cnt = C.log_count;
-      if (!C.drain) ctx->outer_log_hint = cnt;
-      const bool need_order = trace_switch && trace_value;  // integer storage: order only matters for the trace
-      const LogEntry* entries = ctx->log_pin;
-      if (need_order || cnt > pl) {
-        log.resize(static_cast<size_t>(cnt));
-        const int64_t have = std::min<int64_t>(cnt, pl);
-        if (have) std::memcpy(log.data(), ctx->log_pin, sizeof(LogEntry) * have);
-        if (cnt > have) {
-          CK(cpy(ctx, log.data() + have, d.log + have, sizeof(LogEntry) * (cnt - have), cudaMemcpyDeviceToHost,
-                 ctx->stream));
-          CK(cudaStreamSynchronize(ctx->stream));
-        }
-        entries = log.data();
-      }
-      int64_t start = 0;
-      double f_pass = value;
-      std::vector<LogEntry> seg;
-      for (int k = 0; k < passes; ++k) {
-        const int64_t end = C.pass_end[k];
-        f_pass = value;
-        if (need_order) {  // the reference's batch order within the pass
-          seg.assign(entries + start, entries + end);
-          order_log(seg, sorted, 2 * n);
-          for (const auto& L : sorted) {
-            value += L.delta;
-            ++switches;
-            trace.push(switches, value);
-          }
-        } else {  // exact integer partial sums
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          int64_t q = start;
-          for (; q + 4 <= end; q += 4)
-            for (int u = 0; u < 4; ++u) acc[u] += entries[q + u].delta;
-          for (; q < end; ++q) acc[0] += entries[q].delta;
-          value += (acc[0] + acc[1]) + (acc[2] + acc[3]);
-          switches += end - start;
-          trace.len = std::min<int64_t>(kTraceCap, trace.len + (end - start));
-        }
-        start = end;
-        const bool last = k == passes - 1;
-        if (!(last && (C.expired || C.drain)) && trace.len >= kTraceCap) trace.push(switches, value, true);
-      }
-      hmark("log replayed");
-      expired = C.expired != 0;
-      const bool converged = passes > 0 && C.pass_end[passes - 1] == (passes > 1 ? C.pass_end[passes - 2] : 0);
-      if (C.drain && !expired) {  // the log filled up mid-pass: finish that pass host-driven
-        resume_inner = true;
-        resume_f_start = f_pass;
-        begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);
-        ++ctx->launches;
-        CK(cudaGetLastError());
-      } else if (converged || expired) {
-        dev_done = true;
-      } else {  // pass limit / log half full at a pass boundary: the host loop continues
-        begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 0);
-        ++ctx->launches;
-        CK(cudaGetLastError());
-      }
-    }
-  }
-
-  while (!expired && !dev_done) {
+  while (!expired) {
     double f_start = value;  // (first pass: set once the initial objective is read)
-    bool first_pass = !inited;
-    if (resume_inner) {  // continue the pass the device-driven loop left for a log drain
-      resume_inner = false;
-      f_start = resume_f_start;
-      first_pass = false;
-    } else {
+    const bool first_pass = !inited;
     ++S.outer_iterations;
     begin_pass_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctrl_dev, 1);
     ++ctx->launches;
@@ -1552,7 +1346,6 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     S.pair_items += n;
     S.agent_scans += n;
     S.job_scans += n;
-    }
     for (;;) {  // inner loop; repeats only to drain a full delta log
       if (multi && !dist_graph) {
         for (;;) {
@@ -1593,7 +1386,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
             ctx->commit_ms += cms;
             ++ctx->commit_launches;
           }
-          ctx->launches += d.fuse_apply ? 1 : ctx->commit_plan.launches();  // conflict check (+ apply)
+          ctx->launches += ctx->commit_plan.launches();  // conflict check (+ apply)
           rc = run_scan(ctx, 0);
           if (rc) return rc;
           ++launches;
@@ -1662,7 +1455,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       CK(cudaGetLastError());
     }
     if (expired) break;
-    if (P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns) {
+    if (!multi && P.deadline_ns >= 0 && elapsed_ns() >= P.deadline_ns) {
       expired = true;
       break;
     }
@@ -1700,15 +1493,14 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.lfmm_rounds = C.lfmm_rounds - base.lfmm_rounds;
   S.switches_applied = switches;
   const bool graphed = P.use_graph && (!multi || dist_graph);
-  graph_launches += dev_passes;  // each device pass's inner loop ends with one empty batch
   S.scan_launches = graphed ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
   // every body pass of the graph is a commit (conflict check + apply) and a
   // scan launch; the last pass per graph launch finds no active record and
   // exits early
   if (graphed) {
-    const int per_pass = (d.fuse_apply ? 1 : ctx->commit_plan.launches()) +
+    const int per_pass = (ctx->commit_plan.launches()) +
                          (dist_graph ? 2 /* own items */ + 1 /* scan */ + 3 /* push, wait, merge */ : 1);
-    ctx->launches += per_pass * (S.inner_iterations + graph_launches) + 2 * dev_passes;  // + outer begin / end
+    ctx->launches += per_pass * (S.inner_iterations + graph_launches);
   }
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));
   S.terminated_by = expired ? 1 : 0;

@@ -13,29 +13,6 @@ template <class E, int KM>
 cudaError_t launch_scan_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
 template <class E, int KM>
 cudaError_t launch_scan_res_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
-template <class E, int KM>
-cudaError_t launch_scan_cl_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
-template <class E, int KM>
-cudaError_t launch_scan_big_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
-
-// Staged-row + chunk-ring kernel geometry (scan_big.cuh): the whole A row plus
-// two position chunks of (AT, acur, tau16).
-size_t big_smem_bytes(int64_t ld, size_t es, int32_t C) {
-  const size_t row = (static_cast<size_t>(ld) * es + 127) / 128 * 128;
-  const size_t slot = (static_cast<size_t>(C) * (2 * es + 2) + 127) / 128 * 128;
-  return row + 2 * slot + 6 * 8 + 14 * 2 * 16;
-}
-
-// Cluster kernel geometry (scan_cluster.cuh): per CTA a resident tau (int32) and
-// acur slice of L elements and two stages of (A slice, AT slice).
-size_t cl_smem_bytes(int32_t L, size_t es, int CS) {
-  const size_t slice = (static_cast<size_t>(L) * es + 127) / 128 * 128;
-  const size_t tau = (static_cast<size_t>(L) * 4 + 127) / 128 * 128;
-  return tau + slice + 2 * 2 * slice + 10 * 8 + 2 * 15 * 2 * 16 + 2 * CS * 2 * 16;
-}
-
-// Clusters of CS 512-thread CTAs with `smem` bytes each that can be resident at once.
-int cl_active_clusters(int CS, size_t smem);
 
 // Resident-state kernel geometry (scan_resident.cuh): 15 consumer warps + 1
 // producer, tau16 + acur resident, double-buffered (A row, AT row) stages.
@@ -94,16 +71,6 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     if (p.m == 0) {  // one row per CTA does not fit twice: one 512-thread CTA per SM
       p.m = 1;
       p.threads = 512;
-      // LSAPGPU_SCAN_SPLIT=1: stage the gathered row in two half-row passes,
-      // double-buffered (measured 2x slower at C4: every pass scans every
-      // position, so it is off by default).
-      int split = 0;
-      if (const char* sp = std::getenv("LSAPGPU_SCAN_SPLIT")) split = std::atoi(sp);
-      if (split && force_bufs == 0) {
-        p.passes = 2;
-        p.chunk = ((d.ld + 1) / 2 + 63) / 64 * 64;
-        p.bufs = 2;
-      }
     } else {
       p.threads = 256;
     }
@@ -137,42 +104,11 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
   // tracks leave registers for one more stream set), one for integer keys
   p.depth = (d.storage == kF32 || d.storage == kF64) && p.m <= 2 ? 3 : 2;
   if (const char* dd = std::getenv("LSAPGPU_SCAN_DEPTH")) p.depth = std::atoi(dd) == 3 ? 3 : 2;
-  // Cluster kernel (scan_cluster.cuh, opt-in: LSAPGPU_SCAN_CLUSTER=N CTAs per
-  // item): splits each row over N CTAs so rows that cannot be double-buffered
-  // on one SM stream while they are scanned.  Measured on B200 at C4 it is 4x
-  // SLOWER than the streaming kernel (full sweep 11.1 vs 2.77 ms): the random
-  // gathers through distributed shared memory (75 % remote at N = 4) run at
-  // ~1 us each under load.  Kept as a measured alternative, off by default.
-  {
-    int want = 0;
-    if (const char* c = std::getenv("LSAPGPU_SCAN_CLUSTER")) want = std::atoi(c);
-    const bool single_buffered = p.passes > 1 || (p.m == 1 && p.threads == 512 && p.bufs == 1);
-    if (want != 0 && !std::getenv("LSAPGPU_SCAN_BUDGET") && (single_buffered || want > 0)) {
-      const size_t limit = 210 * 1024;
-      for (int cs : {2, 4}) {
-        if (want > 0 && cs != want) continue;
-        int32_t L = static_cast<int32_t>((d.ld + cs - 1) / cs);
-        L = (L + 63) / 64 * 64;
-        const size_t sm = cl_smem_bytes(L, es, cs);
-        if (sm > limit) continue;
-        const int clusters = cl_active_clusters(cs, sm);
-        if (clusters <= 0) continue;
-        p.cluster = cs;
-        p.chunk = L;
-        p.smem = sm;
-        p.ctas = clusters * cs;
-        p.m = 1;
-        p.passes = 1;
-        p.threads = 512;
-        break;
-      }
-    }
-  }
   // Resident-state kernel when tau16 + acur + two (A, AT) stages fit on chip
   // (LSAPGPU_SCAN_RESIDENT=0 forces the streaming kernel).
   int resident = 1;
   if (const char* r = std::getenv("LSAPGPU_SCAN_RESIDENT")) resident = std::atoi(r);
-  if (resident && p.cluster == 0 && d.n < 65536 && d.tau16 && !std::getenv("LSAPGPU_SCAN_BUDGET")) {
+  if (resident && d.n < 65536 && d.tau16 && !std::getenv("LSAPGPU_SCAN_BUDGET")) {
     const size_t limit = 227 * 1024 - 14 * 1024;
     int m = 0;
     for (int mm : {4, 2, 1})
@@ -205,54 +141,10 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       if (p.l2_prefetch >= 32 / m) p.l2_prefetch = 32 / m - 1;
     }
   }
-  // Rows that fit on chip once but not twice (C4): stage the row whole and
-  // stream AT / acur / tau16 through a TMA chunk ring (scan_big.cuh).  Opt-in
-  // (LSAPGPU_SCAN_BIG=1): measured at C4 it is ~10 % slower than the
-  // streaming kernel, whose bound there is the fp64 compare-select work of
-  // float storage, not the stream.
-  int big = 0;
-  if (const char* bg = std::getenv("LSAPGPU_SCAN_BIG")) big = std::atoi(bg);
-  if (big && !p.resident && !p.cluster && d.tau16 && d.n < 65536 && !std::getenv("LSAPGPU_SCAN_BUDGET") &&
-      (p.passes > 1 || (p.m == 1 && p.threads == 512) || big > 1)) {
-    for (int32_t C : {4096, 2048, 1024}) {
-      const size_t sm = big_smem_bytes(d.ld, es, C);
-      if (sm > 210 * 1024) continue;
-      p.big = 1;
-      p.chunk = C;
-      p.smem = sm;
-      p.ctas = num_sms;
-      p.m = 1;
-      p.passes = 1;
-      p.threads = 512;
-      break;
-    }
-  }
   return p;
 }
 
 cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  if (p.big) {
-    switch (d.storage) {
-      case kI16:
-        return d.n <= 16384 ? launch_scan_big_typed<int16_t, kPacked32>(d, p, full, st)
-                            : launch_scan_big_typed<int16_t, kPacked64>(d, p, full, st);
-      case kI32: return launch_scan_big_typed<int32_t, kPacked64>(d, p, full, st);
-      case kF32: return launch_scan_big_typed<float, kFloat>(d, p, full, st);
-      case kF64: return launch_scan_big_typed<double, kFloat>(d, p, full, st);
-      default: return cudaErrorInvalidValue;
-    }
-  }
-  if (p.cluster > 0) {
-    switch (d.storage) {
-      case kI16:
-        return d.n <= 16384 ? launch_scan_cl_typed<int16_t, kPacked32>(d, p, full, st)
-                            : launch_scan_cl_typed<int16_t, kPacked64>(d, p, full, st);
-      case kI32: return launch_scan_cl_typed<int32_t, kPacked64>(d, p, full, st);
-      case kF32: return launch_scan_cl_typed<float, kFloat>(d, p, full, st);
-      case kF64: return launch_scan_cl_typed<double, kFloat>(d, p, full, st);
-      default: return cudaErrorInvalidValue;
-    }
-  }
   if (p.resident) {
     switch (d.storage) {
       case kI16:

@@ -1,11 +1,8 @@
 // Pair-scan instantiations for double storage, key mode 2: the streaming
 // kernel (scan_kernel.cuh) and the resident-state kernel (scan_resident.cuh).
-#include "scan_big.cuh"
-#include "scan_cluster.cuh"
+#include "scan_resident.cuh"
 
 namespace lsapgpu {
 template cudaError_t launch_scan_typed<double, 2>(const DevState&, const ScanPlan&, int, cudaStream_t);
 template cudaError_t launch_scan_res_typed<double, 2>(const DevState&, const ScanPlan&, int, cudaStream_t);
-template cudaError_t launch_scan_big_typed<double, 2>(const DevState&, const ScanPlan&, int, cudaStream_t);
-template cudaError_t launch_scan_cl_typed<double, 2>(const DevState&, const ScanPlan&, int, cudaStream_t);
 }  // namespace lsapgpu

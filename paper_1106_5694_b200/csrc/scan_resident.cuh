@@ -128,28 +128,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
-// Software barrier over the whole (co-resident, one CTA per SM) grid.  The
-// generic-proxy writes before it are made visible to the async proxy (the
-// TMA loads of tau16 / acur / rows after it) on both sides.
-__device__ __forceinline__ void grid_barrier(Ctrl* C) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __threadfence();
-    const uint32_t gen = *reinterpret_cast<volatile uint32_t*>(&C->gbar_gen);
-    if (atomicAdd(&C->gbar_count, 1u) == gridDim.x - 1) {
-      C->gbar_count = 0;
-      __threadfence();
-      atomicAdd(&C->gbar_gen, 1u);
-    } else {
-      while (*reinterpret_cast<volatile uint32_t*>(&C->gbar_gen) == gen) __nanosleep(64);
-    }
-    __threadfence();
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -193,13 +171,6 @@ __global__ void __launch_bounds__(kResThreads, 1)
   pdl_trigger();  // persistent single-wave grid: the next kernel may queue now
   pdl_wait();     // the commit / apply before this scan wrote the state it reads
   if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
-  if (st.fuse_apply && !full) {
-    // the previous commit's scattered writes (commit_apply.cuh) by the whole
-    // persistent grid, then a grid barrier: saves a kernel boundary per batch
-    apply_batch<E>(st, static_cast<int64_t>(blockIdx.x) * blockDim.x + tid, static_cast<int64_t>(gridDim.x) * blockDim.x);
-    grid_barrier(st.ctrl);
-  }
-
   const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
   if (count <= 0) return;
   const uint32_t* __restrict__ items = st.use_own ? st.items_own : st.items;

@@ -72,8 +72,11 @@ struct DevState {
   uint32_t* items_own = nullptr;
   int use_own = 0;
   int emit_edges = 1;
+  // multi-rank solve: the anytime deadline is decided at each record exchange
+  // (every rank's vote travels in its exchange header and the merge ORs them,
+  // dist.cu), never by one rank's commit, so all ranks stop at the same batch
+  int dist_vote = 0;
   int pdl = 0;  // launch the inner-loop kernels with programmatic dependent launch
-  int fuse_apply = 0;  // the resident scan runs the previous commit's apply (no commit_apply_kernel)
   // device timeline (instrumentation): CTA 0 of every scan / commit launch
   // appends (%globaltimer << 4 | kind); null when disabled
   unsigned long long* tl = nullptr;
@@ -118,14 +121,12 @@ struct ScanPlan {
   size_t smem = 0;      // dynamic smem per CTA
   int max_segments = 1;
   int resident = 0;     // 1: resident-state kernel (scan_resident.cuh)
-  int big = 0;          // 1: staged-row + chunk-ring kernel (scan_big.cuh); chunk = positions per chunk
-  int cluster = 0;      // > 0: cluster kernel (scan_cluster.cuh) with this many CTAs per item; chunk = slice
   int depth = 2;        // streaming kernel: vector steps of the streamed rows in flight
   int l2_prefetch = 0;  // resident kernel: stages whose rows are prefetched into L2 ahead
   bool operator==(const ScanPlan& o) const {
     return m == o.m && passes == o.passes && chunk == o.chunk && bufs == o.bufs && ctas == o.ctas &&
            threads == o.threads && smem == o.smem && max_segments == o.max_segments && resident == o.resident &&
-           big == o.big && cluster == o.cluster && depth == o.depth && l2_prefetch == o.l2_prefetch;
+           depth == o.depth && l2_prefetch == o.l2_prefetch;
   }
 };
 ScanPlan plan_scan(const DevState& d, int num_sms);
@@ -161,14 +162,11 @@ struct CommitPlan {
   int cta_edge_cap = 0;     // single-CTA path taken when the proposals fit one CTA (0: never)
   int variant = 0;          // cluster kernel bit 0: read keys before the round-1 atomics
   int wide_keys = 0;        // slot-only LFMM keys cleared every round (n >= 2^17, or LSAPGPU_LFMM_WIDE=1)
-  int fused_apply = 0;      // split commit: the cluster kernel runs the apply itself (1, opt-in:
-                            // measured 7 % slower at C3, 16 SMs of one GPC issue the scattered
-                            // writes) or commit_apply_kernel follows it on 64 SMs (0)
-  int launches() const { return fused_apply ? 1 : 2; }  // kernels per solve-mode commit
+  int launches() const { return 2; }  // kernels per solve-mode commit: conflict check + commit_apply_kernel
   bool operator==(const CommitPlan& o) const {
     return threads == o.threads && smem == o.smem && keys_in_smem == o.keys_in_smem && cluster == o.cluster &&
            cluster_smem == o.cluster_smem && edge_cap == o.edge_cap && cta_edge_cap == o.cta_edge_cap &&
-           variant == o.variant && fused_apply == o.fused_apply && wide_keys == o.wide_keys;
+           variant == o.variant && wide_keys == o.wide_keys;
   }
 };
 CommitPlan plan_commit(const DevState& d);

@@ -371,7 +371,8 @@ class Context:
         p.eps = cfg.improvement_epsilon
         p.reeval = 0 if cfg.reeval == "touched_and_conflicted" else 1
         p.use_graph = 1 if cfg.use_graph else 0
-        p.deadline_ns = -1 if cfg.deadline is None else int(cfg.deadline)
+        # Deadline::starting accepts any budget: zero or negative expires at once
+        p.deadline_ns = -1 if cfg.deadline is None else max(0, int(cfg.deadline))
         p.init_mode = 1 if getattr(cfg, "init", "random") == "greedy" else 0
         if init_sigma is not None:
             init_sigma = np.ascontiguousarray(init_sigma, np.int32)
@@ -383,15 +384,28 @@ class Context:
         ts = np.empty(max(cap, 1), np.int64)
         tv = np.empty(max(cap, 1))
         tl = C.c_int64(0)
-        if dist is None:
-            rc = N.LIB.lsapgpu_solve(self.h, C.byref(p), N.ptr(sigma), N.ptr(tau), C.byref(st),
-                                     N.ptr(ts) if trace else None, N.ptr(tv) if trace else None, cap, C.byref(tl))
-        else:
-            rc = N.LIB.lsapgpu_solve_dist(self.h, C.byref(p), C.byref(dist.struct(self)), N.ptr(sigma),
-                                          N.ptr(tau), C.byref(st), N.ptr(ts) if trace else None,
-                                          N.ptr(tv) if trace else None, cap, C.byref(tl))
-            dist.raise_pending()
-        self._check(rc)
+
+        def run():
+            if dist is None:
+                rc = N.LIB.lsapgpu_solve(self.h, C.byref(p), N.ptr(sigma), N.ptr(tau), C.byref(st),
+                                         N.ptr(ts) if trace else None, N.ptr(tv) if trace else None, cap,
+                                         C.byref(tl))
+            else:
+                rc = N.LIB.lsapgpu_solve_dist(self.h, C.byref(p), C.byref(dist.struct(self)), N.ptr(sigma),
+                                              N.ptr(tau), C.byref(st), N.ptr(ts) if trace else None,
+                                              N.ptr(tv) if trace else None, cap, C.byref(tl))
+                dist.raise_pending()
+            self._check(rc)
+
+        run()
+        if trace and tl.value > cap and cfg.deadline is None and dist is None:
+            # the reference's trace grows by one entry per outer pass past its
+            # 100000 cap (parallel.cpp:15-20,343-344): re-run with room for all
+            # of it (deterministic without a deadline)
+            cap = int(tl.value)
+            ts = np.empty(cap, np.int64)
+            tv = np.empty(cap)
+            run()
         k = min(tl.value, cap)
         rep = SolveReport(
             assignment=Assignment(sigma, tau, st.value),
@@ -428,7 +442,7 @@ class Context:
         p.epsilon = 0.0 if cfg.epsilon is None else float(cfg.epsilon)
         p.scaling = 1 if cfg.scaling else 0
         p.scale_factor = float(cfg.scale_factor)
-        p.deadline_ns = -1 if cfg.deadline is None else int(cfg.deadline)
+        p.deadline_ns = -1 if cfg.deadline is None else max(0, int(cfg.deadline))
         sigma = np.empty(n, np.int32)
         tau = np.empty(n, np.int32)
         prices = np.empty(n)
@@ -562,11 +576,15 @@ def generate_instance(kind: str, n: int, seed: int = 0, param: Optional[float] =
 
 
 def context(device: int = 0) -> Context:
-    """Process-wide default context per device (like the reference's private pool per call)."""
+    """Default context per (host thread, device), like the C++ wrapper's
+    thread_local contexts: ctypes releases the GIL inside the library, so
+    threads sharing one context would interleave set_instance and solve.
+    The reference lets distinct solves run concurrently; so does this."""
+    key = (threading.get_ident(), device)
     with _ctx_lock:
-        c = _contexts.get(device)
+        c = _contexts.get(key)
         if c is None:
-            c = _contexts[device] = Context(device)
+            c = _contexts[key] = Context(device)
         return c
 
 
@@ -576,20 +594,18 @@ def context(device: int = 0) -> Context:
 def dgs_parallel(inst: Instance, cfg: Optional[ParallelConfig] = None) -> SolveReport:
     """lsap::dgs_parallel (parallel.hpp:80) on the B200."""
     cfg = cfg or ParallelConfig()
-    inst.validate()
-    cfg.validate()
     ctx = context(cfg.device)
-    ctx.set_instance(inst)
+    ctx.set_instance(inst)  # Instance::validate (core.cpp:9-15) runs on the device
+    cfg.validate()
     return ctx.solve(cfg)
 
 
 def auction_solve(inst: Instance, cfg: Optional[AuctionConfig] = None, on_round=None) -> SolveReport:
     """lsap::auction_solve (baselines.hpp:33-36) on the B200."""
     cfg = cfg or AuctionConfig()
-    inst.validate()
-    cfg.validate()
     ctx = context(cfg.device)
-    ctx.set_instance(inst)
+    ctx.set_instance(inst)  # Instance::validate on the device
+    cfg.validate()
     return ctx.auction_solve(cfg, on_round=on_round)
 
 
@@ -597,12 +613,11 @@ def evaluate_all_parallel(inst: Instance, asg: Assignment, tables: DeltaTables,
                           cfg: Optional[ParallelConfig] = None) -> None:
     """lsap::evaluate_all_parallel (parallel.hpp:60-61): fills ``tables`` in place."""
     cfg = cfg or ParallelConfig()
-    inst.validate()
+    ctx = context(cfg.device)
+    ctx.set_instance(inst)  # Instance::validate on the device
     cfg.validate()
     if asg.size() != inst.n:
         raise Error("assignment does not match instance")
-    ctx = context(cfg.device)
-    ctx.set_instance(inst)
     t = ctx.evaluate_all(asg.sigma, cfg.improvement_epsilon)
     tables.__dict__.update(t.__dict__)
 
@@ -618,10 +633,9 @@ def apply_parallel_switches(inst: Instance, asg: Assignment, tables: DeltaTables
                             cfg: Optional[ParallelConfig] = None):
     """lsap::apply_parallel_switches (parallel.hpp:71-74) -> (Assignment, [AppliedExchange])."""
     cfg = cfg or ParallelConfig()
-    inst.validate()
+    ctx = context(cfg.device)
+    ctx.set_instance(inst)  # Instance::validate on the device
     cfg.validate()
     if asg.size() != inst.n:
         raise Error("assignment does not match instance")
-    ctx = context(cfg.device)
-    ctx.set_instance(inst)
     return ctx.apply_parallel_switches(asg, tables, sets, cfg.improvement_epsilon)

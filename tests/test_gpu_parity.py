@@ -113,20 +113,13 @@ def test_generators_match_oracle(oracle, gpu_ctx):
 @pytest.mark.parametrize("env", [
     {},                                                                # resident-state kernel (default)
     {"LSAPGPU_COMMIT_SINGLE": "0"},                                    # cluster commit for every batch
-    {"LSAPGPU_COMMIT_FUSED_APPLY": "1"},                               # apply inside the cluster kernel
-    {"LSAPGPU_COMMIT_FUSED_APPLY": "1", "LSAPGPU_COMMIT_SINGLE": "0"},
-    {"LSAPGPU_FUSE_APPLY": "1"},                                       # apply inside the resident scan
-    {"LSAPGPU_DEVICE_OUTER": "1"},                                     # whole solve as one graph (opt-in)
     {"LSAPGPU_LFMM_WIDE": "1", "LSAPGPU_COMMIT_SINGLE": "0"},            # round-cleared LFMM keys (the n >= 2^17 path)
     {"LSAPGPU_SCAN_M": "1", "LSAPGPU_SCAN_BUFS": "4"},                # resident, 4-deep stage ring
     {"LSAPGPU_SCAN_M": "4"},                                           # resident, 4 items per stage
     {"LSAPGPU_SCAN_SEGMENTS": "8"},                                    # resident, items split over CTAs
-    {"LSAPGPU_SCAN_CLUSTER": "2"},                                     # row split over a 2-CTA cluster (opt-in)
-    {"LSAPGPU_SCAN_CLUSTER": "4"},                                     # ... 4 CTAs
-    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_BIG": "2"},          # staged row + TMA chunk ring (opt-in)
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "1"},             # streaming kernel
-    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_BIG": "0", "LSAPGPU_SCAN_M": "2"},
-    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_BIG": "0", "LSAPGPU_SCAN_M": "4"},
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "2"},
+    {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_M": "4"},
     {"LSAPGPU_SCAN_BUDGET": "3072"},                                   # streaming, chunked passes
     {"LSAPGPU_SCAN_BUDGET": "9000", "LSAPGPU_SCAN_M": "1"},            # streaming, single-buffered rows
     {"LSAPGPU_SCAN_RESIDENT": "0", "LSAPGPU_SCAN_SEGMENTS": "8"},      # streaming, split items
