@@ -99,7 +99,9 @@ typedef struct {
   int64_t scan_launches;
   int64_t bytes_scanned;      /* algorithmic HBM bytes of the pair scans: pair_items * 2 * n * elem */
   int32_t storage;            /* LSAPGPU_STORE_* */
-  int32_t pad_;
+  int32_t scan_filter;        /* 0, or 8 / 16: the long-row scan's quantized filter copies */
+  int64_t filter_kept;        /* filter scan: candidates verified exactly (all items of the solve) */
+  int64_t filter_overflows;   /* filter scan: items verified by a whole-row exact scan (queue overflow) */
 } lsapgpu_stats;
 
 const char* lsapgpu_version(void);
@@ -264,6 +266,13 @@ int lsapgpu_set_scan_timing(lsapgpu_ctx* ctx, int enabled);
 int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
                         double* full_sweep_ms, int64_t* full_sweeps, double* commit_ms,
                         int64_t* commit_launches);
+
+/* The pair-scan plan chosen for the current matrix (instrumentation): up to
+ * cap of {kernel (0 streaming, 1 resident, 2 quantized filter), items or row
+ * buffers per CTA, stage buffers or chunk slots, filter bits (0, 8, 16), CTAs,
+ * threads per CTA, dynamic smem bytes, chunk, filter queue capacity}.
+ * Returns the number of values written, < 0 on error. */
+int lsapgpu_scan_plan(const lsapgpu_ctx* ctx, int32_t* info, int32_t cap);
 
 /* Device timeline (instrumentation, off by default): with capacity > 0 the
  * first CTA of every pair-scan and commit launch appends one entry

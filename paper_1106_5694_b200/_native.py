@@ -26,7 +26,7 @@ EXPORTS = [
     "lsapgpu_generate", "lsapgpu_n", "lsapgpu_storage", "lsapgpu_read_rows", "lsapgpu_solve",
     "lsapgpu_evaluate_all", "lsapgpu_check_conflicts", "lsapgpu_apply_parallel_switches",
     "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_solve_dist",
-    "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing",
+    "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing", "lsapgpu_scan_plan",
     "lsapgpu_set_timeline", "lsapgpu_timeline", "lsapgpu_auction_solve",
     "lsapgpu_greedy_assignment",
     "lsapgpu_dist_p2p_bytes", "lsapgpu_ipc_handle", "lsapgpu_ipc_open", "lsapgpu_ipc_close",
@@ -62,7 +62,9 @@ class Stats(C.Structure):
         ("scan_launches", C.c_int64),
         ("bytes_scanned", C.c_int64),
         ("storage", C.c_int32),
-        ("pad_", C.c_int32),
+        ("scan_filter", C.c_int32),
+        ("filter_kept", C.c_int64),
+        ("filter_overflows", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -92,7 +94,9 @@ class AuctionStats(C.Structure):
         ("epsilon", C.c_double),
         ("bytes_scanned", C.c_int64),
         ("storage", C.c_int32),
-        ("pad_", C.c_int32),
+        ("scan_filter", C.c_int32),
+        ("filter_kept", C.c_int64),
+        ("filter_overflows", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -161,6 +165,7 @@ def _load() -> C.CDLL:
         "lsapgpu_auction_solve": (C.c_int, [vp, C.POINTER(AuctionParams), vp, vp, C.POINTER(AuctionStats),
                                             vp, vp, i64]),
         "lsapgpu_greedy_assignment": (C.c_int, [vp, vp, C.POINTER(i64)]),
+        "lsapgpu_scan_plan": (C.c_int, [vp, vp, C.c_int32]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
                                           C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),
     }

@@ -2,7 +2,7 @@
 
     python -m paper_1106_5694_b200.build [--force]
 
-Compiles csrc/*.cu in parallel to objects under build/ and links
+Compiles csrc/*.cu (nvcc) and csrc/*.cpp (host compiler) in parallel to objects under build/ and links
 paper_1106_5694_b200/lib/liblsapgpu.so.  Rebuilds only when a source or header
 is newer than the library.
 """
@@ -35,7 +35,14 @@ def nvcc() -> str:
 
 
 def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu"))) + sorted(glob.glob(os.path.join(CSRC, "*.cpp")))
+
+
+def gxx() -> str:
+    for c in (os.environ.get("CXX"), shutil.which("g++")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("g++ not found")
 
 
 def deps():
@@ -51,12 +58,15 @@ def up_to_date() -> bool:
 
 
 def _compile(src: str) -> tuple:
-    obj = os.path.join(OBJ_DIR, os.path.basename(src).replace(".cu", ".o"))
+    obj = os.path.join(OBJ_DIR, os.path.basename(src).rsplit(".", 1)[0] + ".o")
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         [os.path.join(ROOT, "include", "lsapgpu.h")]
     if os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in [src, *headers]):
         return src, obj, 0, open(obj + ".ptxas.txt").read() if os.path.exists(obj + ".ptxas.txt") else ""
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    if src.endswith(".cpp"):  # host-only code (AVX2 intrinsics): the host compiler directly
+        cmd = [gxx(), "-O2", "-std=c++17", "-fPIC", "-c", src, "-o", obj]
+    else:
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, r.returncode, r.stdout + r.stderr
 

@@ -110,6 +110,9 @@ struct Ctrl {
   uint32_t push_done;  // CTAs finished with the peer push of the current round
   uint32_t pad2_;
   uint64_t p2p_epoch;  // peer transport: rounds pushed (flags carry it; graph-capturable)
+  // quantized-filter scan (instrumentation): candidates verified exactly,
+  // items that overflowed their queue (whole-item exact fallback)
+  int64_t filter_kept, filter_overflows;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

@@ -185,7 +185,7 @@ struct Pair<double> {
 
 template <class E>
 __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0, int64_t rows, E* A, E* AT,
-                                                           int64_t ld, uint32_t* flags) {
+                                                           int64_t ld, uint32_t* flags, uint32_t* amax) {
   __shared__ E tile[64][66];
   const int64_t bi = row0 + static_cast<int64_t>(blockIdx.y) * 64;  // agent block
   const int64_t bj = static_cast<int64_t>(blockIdx.x) * 64;         // job block
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
   const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;  // 8 row groups
   const int64_t j = bj + 2 * lane;
   uint32_t f = 0;
+  float vmax = 0.f;  // max |entry| rounded up to fp32 (the filter scan's quantization scale)
   // all eight rows' loads first (8 x 16 B in flight per lane), then classify / store
   double v[8][2];
   const bool fast = src.s.kind == 0 && src.s.src_dtype == 0 && j + 1 < n && (n & 1) == 0;
@@ -219,6 +220,10 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
     const double v0 = v[q][0], v1 = v[q][1];
     if (j < n) f |= entry_flags(v0);
     if (j + 1 < n) f |= entry_flags(v1);
+    if (amax) {
+      if (j < n && isfinite(v0)) vmax = fmaxf(vmax, __double2float_ru(fabs(v0)));
+      if (j + 1 < n && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
+    }
     const E e0 = narrow<E>(isfinite(v0) ? v0 : 0.0), e1 = narrow<E>(isfinite(v1) ? v1 : 0.0);
     if (j + 1 < n)
       Pair<E>::st(A + i * ld + j, e0, e1);
@@ -241,12 +246,56 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
   }
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
   __shared__ uint32_t wf[8];
+  __shared__ float wm[8];
   if (lane == 0) wf[rg] = f;
+  if (amax) {
+    for (int off = 16; off > 0; off >>= 1) vmax = fmaxf(vmax, __shfl_down_sync(0xffffffffu, vmax, off));
+    if (lane == 0) wm[rg] = vmax;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t r = 0;
     for (int w = 0; w < 8; ++w) r |= wf[w];
     if (r) atomicOr(flags, r);
+    if (amax) {
+      float m = 0.f;
+      for (int w = 0; w < 8; ++w) m = fmaxf(m, wm[w]);
+      if (m > 0.f) atomicMax(amax, __float_as_uint(m));  // non-negative floats order as their bits
+    }
+  }
+}
+
+// Filter copies (scan_filter.cuh): Q = ceil(A * scale) as int16 / int8, an
+// upper bound of every entry in units of 1/scale (scale is a power of two, so
+// the product is exact in fp64 and so is the ceiling); padding columns 0.
+template <class E, class Qt>
+__global__ void quantize_kernel(const E* __restrict__ src, Qt* __restrict__ dst, int64_t total, int32_t n,
+                                int64_t ld, double scale) {
+  for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8; k < total;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x * 8) {
+    const int64_t col = k % ld;  // ld is a multiple of 64: the 8 elements share a row
+    Qt out[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      out[e] = col + e < n ? static_cast<Qt>(ceil(static_cast<double>(src[k + e]) * scale)) : Qt(0);
+    if constexpr (sizeof(Qt) == 2) {
+      uint4 w;
+      w.x = static_cast<uint16_t>(out[0]) | (static_cast<uint32_t>(static_cast<uint16_t>(out[1])) << 16);
+      w.y = static_cast<uint16_t>(out[2]) | (static_cast<uint32_t>(static_cast<uint16_t>(out[3])) << 16);
+      w.z = static_cast<uint16_t>(out[4]) | (static_cast<uint32_t>(static_cast<uint16_t>(out[5])) << 16);
+      w.w = static_cast<uint16_t>(out[6]) | (static_cast<uint32_t>(static_cast<uint16_t>(out[7])) << 16);
+      *reinterpret_cast<uint4*>(dst + k) = w;
+    } else {
+      uint2 w;
+      w.x = 0;
+      w.y = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        w.x |= static_cast<uint32_t>(static_cast<uint8_t>(out[e])) << (8 * e);
+        w.y |= static_cast<uint32_t>(static_cast<uint8_t>(out[4 + e])) << (8 * e);
+      }
+      *reinterpret_cast<uint2*>(dst + k) = w;
+    }
   }
 }
 
@@ -307,8 +356,21 @@ struct BuildK {
 template <class E>
 struct FusedK {
   static void run(dim3 g, dim3 b, cudaStream_t st, Src s, int64_t r0, int64_t rows, void* A, void* AT,
-                  int64_t ld, uint32_t* flags) {
-    layout_fused_kernel<E><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags);
+                  int64_t ld, uint32_t* flags, uint32_t* amax) {
+    layout_fused_kernel<E><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags,
+                                           amax);
+  }
+};
+template <class E>
+struct QuantK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, const void* src, void* dst, int64_t total, int32_t n,
+                  int64_t ld, double scale, int qbits) {
+    if (qbits == 16)
+      quantize_kernel<E, int16_t><<<g, b, 0, st>>>(static_cast<const E*>(src), static_cast<int16_t*>(dst), total, n,
+                                                   ld, scale);
+    else
+      quantize_kernel<E, int8_t><<<g, b, 0, st>>>(static_cast<const E*>(src), static_cast<int8_t*>(dst), total, n,
+                                                  ld, scale);
   }
 };
 template <class E>
@@ -357,10 +419,18 @@ cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, 
 }
 
 cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
-                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st) {
+                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st, uint32_t* amax) {
   Src src{s, n};
   dim3 g(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
-  return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags);
+  return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags, amax);
+}
+
+cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(d.n) * d.ld;
+  const dim3 g(148 * 8), b(256);
+  cudaError_t e = dispatch<QuantK>(d.storage, g, b, st, d.A, Q, total, d.n, d.ld, scale, qbits);
+  if (e != cudaSuccess) return e;
+  return dispatch<QuantK>(d.storage, g, b, st, d.AT, QT, total, d.n, d.ld, scale, qbits);
 }
 
 cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st) {

@@ -19,6 +19,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <thread>
 #include <vector>
 
@@ -26,6 +27,14 @@
 #include "state.h"
 
 using namespace lsapgpu;
+
+namespace lsapgpu {
+// Exact host narrowing (host_narrow.cpp, AVX2): false if any value is not
+// representable under the storage rule (or is not finite).
+bool narrow_to_i16(const double* src, int16_t* dst, size_t cnt);
+bool narrow_to_i32(const double* src, int32_t* dst, size_t cnt);
+bool narrow_to_f32(const double* src, float* dst, size_t cnt);
+}  // namespace lsapgpu
 
 namespace {
 
@@ -77,7 +86,7 @@ constexpr size_t kStageKeep = 16ull << 30;     // keep the device staging copy u
 int upload_threads() {
   if (const char* e = std::getenv("LSAPGPU_UPLOAD_THREADS")) return std::max(1, std::atoi(e));
   const unsigned hw = std::thread::hardware_concurrency();
-  return static_cast<int>(std::max(2u, std::min(8u, hw ? hw / 2 : 2u)));
+  return static_cast<int>(std::max(2u, std::min(16u, hw ? hw : 2u)));
 }
 
 // Fixed pool of host threads for the pageable -> pinned copies: run(fn) calls
@@ -151,6 +160,7 @@ struct lsapgpu_ctx {
   int32_t n_matrix = 0;   // matrix present for this n (0 = none)
   std::vector<Buf> vec_bufs;
   Buf mat;                // A and AT (one allocation)
+  Buf qmat;               // Q and QT: quantized filter copies (scan_filter.cuh), when the plan uses them
   Ctrl* ctrl_dev = nullptr;
   Ctrl* ctrl_host = nullptr;  // pinned mirror
   uint32_t* flags_dev = nullptr;
@@ -316,6 +326,7 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.rej_stamp, N2, true));
   CK(valloc(ctx, &d.items, N, false));
   CK(valloc(ctx, &d.items_own, N, false));
+  CK(valloc(ctx, &d.aux, N, true));
   d.log_cap = std::max<int64_t>(1 << 20, 8 * static_cast<int64_t>(n));
   CK(valloc(ctx, &d.log, static_cast<size_t>(d.log_cap), false));
   d.part_cap = (static_cast<int64_t>(n) + 8) * 16;
@@ -369,11 +380,59 @@ int alloc_matrix(lsapgpu_ctx* ctx, int32_t n, int storage) {
   return LSAPGPU_OK;
 }
 
-void finish_matrix(lsapgpu_ctx* ctx, int32_t n) {
+// Quantized filter copies for the long-row scan (scan_filter.cuh): a
+// power-of-two scale with max|a| * scale <= 16383 (int16) or 127 (int8), from
+// the max the layout pass reduced into flags_dev[2], then Q / QT.
+int build_filter_copies(lsapgpu_ctx* ctx) {
+  DevState& d = ctx->d;
+  const ScanPlan& p = ctx->scan_plan;
+  uint32_t bits = 0;
+  CK(cpy(ctx, &bits, ctx->flags_dev + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float amax = 0.f;
+  std::memcpy(&amax, &bits, sizeof(amax));
+  const double limit = p.filter == 16 ? 16383.0 : 127.0;
+  double scale = 1.0;
+  if (amax > 0.f) {
+    int e = 0;
+    std::frexp(limit / static_cast<double>(amax), &e);  // limit / amax in [2^(e-1), 2^e)
+    scale = std::ldexp(1.0, std::max(-1000, std::min(1000, e - 1)));
+    while (static_cast<double>(amax) * scale > limit) scale *= 0.5;
+  }
+  const size_t qb = p.filter / 8;
+  const size_t bytes = static_cast<size_t>(d.n) * static_cast<size_t>(d.ld) * qb;
+  if (ctx->qmat.bytes < 2 * bytes) {
+    if (ctx->qmat.p) cudaFree(ctx->qmat.p);
+    ctx->qmat.p = nullptr;
+    ctx->qmat.bytes = 0;
+    CK(cudaMalloc(&ctx->qmat.p, 2 * bytes));
+    ctx->qmat.bytes = 2 * bytes;
+  }
+  d.Q = ctx->qmat.p;
+  d.QT = static_cast<unsigned char*>(ctx->qmat.p) + bytes;
+  d.qscale = scale;
+  CK(launch_quantize(d, p.filter, scale, const_cast<void*>(d.Q), const_cast<void*>(d.QT), ctx->stream));
+  ctx->launches += 2;
+  return LSAPGPU_OK;
+}
+
+int finish_matrix(lsapgpu_ctx* ctx, int32_t n) {
   ctx->scan_plan = plan_scan(ctx->d, ctx->num_sms);
   ctx->commit_plan = plan_commit(ctx->d);
+  DevState& d = ctx->d;
+  d.Q = d.QT = nullptr;
+  d.qscale = 0.0;
+  if (ctx->scan_plan.filter) {
+    const int rc = build_filter_copies(ctx);
+    if (rc) return rc;
+  } else if (ctx->qmat.p) {  // free the copies of a previous matrix
+    cudaFree(ctx->qmat.p);
+    ctx->qmat.p = nullptr;
+    ctx->qmat.bytes = 0;
+  }
   ctx->n_matrix = n;
   ctx->range_ok = false;
+  return LSAPGPU_OK;
 }
 
 // Builds A/AT from a layout source; src_rows_dev is a device pointer for memory sources.
@@ -384,7 +443,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   int rc = ensure_vectors(ctx, n);
   if (rc) return rc;
   ctx->n_matrix = 0;
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, 2 * sizeof(uint32_t), ctx->stream));
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, 3 * sizeof(uint32_t), ctx->stream));
   const int64_t probe = std::min<int64_t>(64, n);
   CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream));
   ++ctx->launches;
@@ -396,7 +455,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   if ((rc = alloc_matrix(ctx, n, spec))) return rc;
   DevState& d = ctx->d;
   CK(launch_layout_fused(src, n, 0, n, spec, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
-                         ctx->flags_dev + 1, ctx->stream));
+                         ctx->flags_dev + 1, ctx->stream, ctx->flags_dev + 2));
   ++ctx->launches;
   CK(cpy(ctx, &flags, ctx->flags_dev + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -409,8 +468,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
     ++ctx->launches;
     CK(cudaStreamSynchronize(ctx->stream));
   }
-  finish_matrix(ctx, n);
-  return LSAPGPU_OK;
+  return finish_matrix(ctx, n);
 }
 
 // Host upload (lsapgpu_set_matrix): the matrix crosses PCIe in row chunks
@@ -422,10 +480,154 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
 // the rest pay for that).  Pageable host memory is first copied into a ring
 // of pinned buffers by a pool of host threads, so it streams at close to the
 // pinned PCIe rate instead of the driver's single-threaded pageable path.
+// Host-side classification of fp64 entries, the rules of the device's
+// entry_flags (layout.cu): bit0 non-finite, bit1 not int16-exact, bit2 not an
+// integer below 2^29, bit3 not fp32-exact.
+uint32_t host_entry_flags(double v) {
+  if (!std::isfinite(v)) return 15u;
+  uint32_t f = 0;
+  const bool i16 = v >= -32767.0 && v <= 32767.0 && static_cast<double>(static_cast<int32_t>(v)) == v;
+  if (!i16) f |= 2u;
+  const bool i32 = v > -536870912.0 && v < 536870912.0 && static_cast<double>(static_cast<int32_t>(v)) == v;
+  if (!i32) f |= 4u;
+  if (std::fabs(v) > 3.4028234663852886e38 || static_cast<double>(static_cast<float>(v)) != v) f |= 8u;
+  return f;
+}
+
+inline bool narrow_block(const double* src, int16_t* dst, size_t cnt) { return lsapgpu::narrow_to_i16(src, dst, cnt); }
+inline bool narrow_block(const double* src, int32_t* dst, size_t cnt) { return lsapgpu::narrow_to_i32(src, dst, cnt); }
+inline bool narrow_block(const double* src, float* dst, size_t cnt) { return lsapgpu::narrow_to_f32(src, dst, cnt); }
+
+constexpr int kNarrowFallback = 1000;  // upload_narrow: a value needs a wider type; redo as fp64
+
+// The host upload with the matrix narrowed on the HOST (pool threads convert
+// each chunk into the pinned ring as int16 / int32 / fp32, the storage type
+// speculated from the first 64 rows): PCIe then carries 2 or 4 bytes per
+// entry instead of 8, and the device builds A / AT from the narrow staging
+// copy exactly as from fp64 (the narrowing is exact).  Any value that does
+// not fit returns kNarrowFallback and the caller redoes the fp64 upload.
+template <class T>
+int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, int32_t ndtype) {
+  const size_t row_bytes = static_cast<size_t>(n) * sizeof(T);
+  const size_t total = row_bytes * static_cast<size_t>(n);
+  if (ctx->stage.bytes < total) {
+    if (ctx->stage.p) cudaFree(ctx->stage.p);
+    ctx->stage.p = nullptr;
+    ctx->stage.bytes = 0;
+    CK(cudaMalloc(&ctx->stage.p, total));
+    ctx->stage.bytes = total;
+  }
+  // chunks of ~64 MB of SOURCE (fp64) rows, as the fp64 path
+  int64_t chunk_rows = static_cast<int64_t>(kUploadChunk / (static_cast<size_t>(n) * 8)) / 32 * 32;
+  if (chunk_rows < 32) chunk_rows = 32;
+  if (chunk_rows > n) chunk_rows = n;
+  const int nchunks = static_cast<int>((n + chunk_rows - 1) / chunk_rows);
+  if (static_cast<int>(ctx->chunk_flags_cap) < nchunks) {
+    if (ctx->chunk_flags) cudaFree(ctx->chunk_flags);
+    ctx->chunk_flags = nullptr;
+    ctx->chunk_flags_cap = 0;
+    CK(cudaMalloc(&ctx->chunk_flags, sizeof(uint32_t) * nchunks));
+    ctx->chunk_flags_cap = nchunks;
+  }
+  CK(cudaMemsetAsync(ctx->chunk_flags, 0, sizeof(uint32_t) * nchunks, ctx->stream));
+  CK(cudaMemsetAsync(ctx->flags_dev + 2, 0, sizeof(uint32_t), ctx->stream));  // max |a| (filter scale)
+  CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_ready, 0));
+  const size_t ring_bytes = static_cast<size_t>(chunk_rows) * row_bytes;
+  if (ctx->ring_bytes < ring_bytes) {
+    for (auto& r : ctx->ring)
+      if (r) cudaFreeHost(r);
+    for (auto& r : ctx->ring) r = nullptr;
+    ctx->ring_bytes = 0;
+    for (auto& r : ctx->ring) CK(cudaMallocHost(&r, ring_bytes));
+    ctx->ring_bytes = ring_bytes;
+  }
+  if (!ctx->pool) ctx->pool = new HostPool(upload_threads());
+  {
+    const int rc = alloc_matrix(ctx, n, storage);
+    if (rc) return rc;
+  }
+  LayoutSource src;
+  src.kind = 0;
+  src.src = ctx->stage.p;
+  src.src_dtype = ndtype;
+  const int T_ = ctx->pool->size();
+  std::vector<uint8_t> okv(static_cast<size_t>(T_));
+  for (int k = 0; k < nchunks; ++k) {
+    const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
+    const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
+    const size_t cnt = static_cast<size_t>(rows) * static_cast<size_t>(n);
+    const int b = k % kRing;
+    if (k >= kRing) CK(cudaEventSynchronize(ctx->ev_chunk[b]));  // ring slot's previous DMA done
+    T* pin = static_cast<T*>(ctx->ring[b]);
+    const double* hsrc = data + static_cast<size_t>(r0) * static_cast<size_t>(n);
+    ctx->pool->run([&](int t) {
+      const size_t a = cnt * t / T_, e = cnt * (t + 1) / T_;
+      okv[t] = narrow_block(hsrc + a, pin + a, e - a) ? 1 : 0;
+    });
+    for (int t = 0; t < T_; ++t)
+      if (!okv[t]) {
+        CK(cudaStreamSynchronize(ctx->copy_stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return kNarrowFallback;
+      }
+    unsigned char* dst = static_cast<unsigned char*>(ctx->stage.p) + static_cast<size_t>(r0) * row_bytes;
+    CK(cpy(ctx, dst, pin, cnt * sizeof(T), cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->ev_chunk[b], ctx->copy_stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_chunk[b], 0));
+    CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
+                           ctx->d.ld, ctx->chunk_flags + k, ctx->stream, ctx->flags_dev + 2));
+    ++ctx->launches;
+  }
+  std::vector<uint32_t> fl(nchunks);
+  CK(cpy(ctx, fl.data(), ctx->chunk_flags, sizeof(uint32_t) * nchunks, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  uint32_t all = 0;
+  for (uint32_t f : fl) all |= f;
+  const int final_storage = storage_of_flags(all);
+  if (final_storage != storage) {  // (cannot widen: every value passed T's rule; narrower is possible)
+    int rc = alloc_matrix(ctx, n, final_storage);
+    if (rc) return rc;
+    CK(launch_build_layout(src, n, 0, n, final_storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
+                           ctx->d.ld, ctx->stream));
+    ++ctx->launches;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  if (total > kStageKeep) {
+    cudaFree(ctx->stage.p);
+    ctx->stage.p = nullptr;
+    ctx->stage.bytes = 0;
+  }
+  return finish_matrix(ctx, n);
+}
+
 int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
   int rc = ensure_vectors(ctx, n);
   if (rc) return rc;
   ctx->n_matrix = 0;
+  static const bool narrow_env = !(std::getenv("LSAPGPU_HOST_NARROW") && std::atoi(std::getenv("LSAPGPU_HOST_NARROW")) == 0);
+  if (dtype == LSAPGPU_F64 && narrow_env) {
+    // speculate the storage from the first rows on the host
+    const double* a = static_cast<const double*>(data);
+    const size_t probe = static_cast<size_t>(std::min<int32_t>(64, n)) * static_cast<size_t>(n);
+    if (!ctx->pool) ctx->pool = new HostPool(upload_threads());
+    const int T_ = ctx->pool->size();
+    std::vector<uint32_t> pf(static_cast<size_t>(T_), 0u);
+    ctx->pool->run([&](int t) {
+      uint32_t f = 0;
+      for (size_t i = probe * t / T_; i < probe * (t + 1) / T_; ++i) f |= host_entry_flags(a[i]);
+      pf[t] = f;
+    });
+    uint32_t f = 0;
+    for (uint32_t x : pf) f |= x;
+    if (f & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+    const int spec = storage_of_flags(f);
+    rc = kNarrowFallback;
+    if (spec == kI16) rc = upload_narrow<int16_t>(ctx, a, n, kI16, LSAPGPU_I16);
+    else if (spec == kI32) rc = upload_narrow<int32_t>(ctx, a, n, kI32, LSAPGPU_I32);
+    else if (spec == kF32) rc = upload_narrow<float>(ctx, a, n, kF32, LSAPGPU_F32);
+    if (rc != kNarrowFallback) return rc;
+  }
   const size_t es = src_size(dtype);
   const size_t row_bytes = static_cast<size_t>(n) * es;
   const size_t total = row_bytes * static_cast<size_t>(n);
@@ -449,6 +651,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
     ctx->chunk_flags_cap = nchunks;
   }
   CK(cudaMemsetAsync(ctx->chunk_flags, 0, sizeof(uint32_t) * nchunks, ctx->stream));
+  CK(cudaMemsetAsync(ctx->flags_dev + 2, 0, sizeof(uint32_t), ctx->stream));  // max |a| (filter scale)
   CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_ready, 0));
 
@@ -512,7 +715,8 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
       }
     }
     CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
-                           const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->chunk_flags + k, ctx->stream));
+                           const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->chunk_flags + k, ctx->stream,
+                           ctx->flags_dev + 2));
     ++ctx->launches;
   }
   std::vector<uint32_t> fl(nchunks);
@@ -534,8 +738,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
     ctx->stage.p = nullptr;
     ctx->stage.bytes = 0;
   }
-  finish_matrix(ctx, n);
-  return LSAPGPU_OK;
+  return finish_matrix(ctx, n);
 }
 
 bool is_perm(const int32_t* p, int32_t n) {
@@ -672,7 +875,7 @@ int build_dist_graph(lsapgpu_ctx* ctx, const PeerSet& ps) {
 int run_scan(lsapgpu_ctx* ctx, int full) {
   if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(launch_scan(ctx->d, ctx->scan_plan, full, ctx->stream));
-  ++ctx->launches;
+  ctx->launches += ctx->scan_plan.launches();
   if (ctx->timing) {
     CK(cudaEventRecord(ctx->ev1, ctx->stream));
     CK(cudaEventSynchronize(ctx->ev1));
@@ -759,7 +962,7 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||
-      cudaMalloc(&ctx->flags_dev, 2 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&ctx->flags_dev, 4 * sizeof(uint32_t)) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming) != cudaSuccess) {
@@ -788,6 +991,7 @@ void lsapgpu_destroy(lsapgpu_ctx* ctx) {
   if (ctx->dist_graph) cudaGraphDestroy(ctx->dist_graph);
   free_vectors(ctx);
   if (ctx->mat.p) cudaFree(ctx->mat.p);
+  if (ctx->qmat.p) cudaFree(ctx->qmat.p);
   if (ctx->ctrl_dev) cudaFree(ctx->ctrl_dev);
   if (ctx->ctrl_host) cudaFreeHost(ctx->ctrl_host);
   if (ctx->flags_dev) cudaFree(ctx->flags_dev);
@@ -952,6 +1156,16 @@ int32_t lsapgpu_timeline(lsapgpu_ctx* ctx, uint64_t* out, int32_t capacity) {
   push_ctrl(ctx);
   cudaStreamSynchronize(ctx->stream);
   return cnt;
+}
+
+int lsapgpu_scan_plan(const lsapgpu_ctx* ctx, int32_t* info, int32_t cap) {
+  if (!ctx || !info || cap < 0) return LSAPGPU_ERR_INVALID;
+  const ScanPlan& p = ctx->scan_plan;
+  const int32_t v[9] = {p.filter ? 2 : (p.resident ? 1 : 0), p.m, p.bufs, p.filter, p.ctas, p.threads,
+                        static_cast<int32_t>(p.smem), static_cast<int32_t>(p.chunk), p.filter_queue};
+  const int32_t k = cap < 9 ? cap : 9;
+  for (int32_t q = 0; q < k; ++q) info[q] = v[q];
+  return k;
 }
 
 int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launches,
@@ -1216,8 +1430,21 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     DevState ds = d;
     ds.use_own = 1;
     ds.emit_edges = 0;
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev0, ctx->stream));
     CK(launch_scan(ds, ctx->scan_plan, 0, ctx->stream));
-    ++ctx->launches;
+    ctx->launches += ctx->scan_plan.launches();
+    if (ctx->timing) {  // this rank's scan of its share (host-stepped solves with timing on)
+      CK(cudaEventRecord(ctx->ev1, ctx->stream));
+      CK(cudaEventSynchronize(ctx->ev1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      ctx->scan_ms += ms;
+      ++ctx->scan_launches;
+      if (full) {
+        ctx->full_ms += ms;
+        ++ctx->full_launches;
+      }
+    }
     if (p2p) {  // pack + allgather in one kernel over peer memory, then wait + merge
       CK(launch_dist_push(d, ps, ctx->stream));
       ctx->launches += 3;
@@ -1491,6 +1718,9 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.agent_scans += C.agent_scans - base.agent_scans;
   S.job_scans += C.job_scans - base.job_scans;
   S.lfmm_rounds = C.lfmm_rounds - base.lfmm_rounds;
+  S.scan_filter = ctx->scan_plan.filter;
+  S.filter_kept = C.filter_kept - base.filter_kept;
+  S.filter_overflows = C.filter_overflows - base.filter_overflows;
   S.switches_applied = switches;
   const bool graphed = P.use_graph && (!multi || dist_graph);
   S.scan_launches = graphed ? S.outer_iterations + S.inner_iterations + graph_launches : launches;
@@ -1499,7 +1729,8 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   // exits early
   if (graphed) {
     const int per_pass = (ctx->commit_plan.launches()) +
-                         (dist_graph ? 2 /* own items */ + 1 /* scan */ + 3 /* push, wait, merge */ : 1);
+                         (dist_graph ? 2 /* own items */ + 3 /* push, wait, merge */ : 0) +
+                         ctx->scan_plan.launches();
     ctx->launches += per_pass * (S.inner_iterations + graph_launches);
   }
   S.bytes_scanned = S.pair_items * 2 * static_cast<int64_t>(n) * static_cast<int64_t>(esize(d.storage));

@@ -1,5 +1,6 @@
 // scan.cu -- scan plan and dispatch for the fused pair-scan kernel
 // (scan_kernel.cuh; instantiated per storage type in scan_<type>.cu).
+#include <algorithm>
 #include <cstdlib>
 
 #include "state.h"
@@ -13,6 +14,18 @@ template <class E, int KM>
 cudaError_t launch_scan_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
 template <class E, int KM>
 cudaError_t launch_scan_res_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+template <class E>
+cudaError_t launch_scan_filter_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st);
+
+// Quantized-filter kernel geometry (scan_filter.cuh): row buffers of the
+// quantized A rows, a ring of QT chunk slots, two candidate queues.
+constexpr int32_t kFilterChunk = 4096;
+constexpr int kFilterQueueMax = 1024;
+size_t filter_smem(int64_t ld, int qbytes, int rb, int ns, int qcap) {
+  const size_t row = (static_cast<size_t>(ld) * qbytes + 127) / 128 * 128;
+  const size_t slot = static_cast<size_t>(kFilterChunk) * qbytes;
+  return rb * row + ns * slot + 2 * static_cast<size_t>(qcap) * 8 + (rb + 2 * 8 + 4) * 8;
+}
 
 // Resident-state kernel geometry (scan_resident.cuh): 15 consumer warps + 1
 // producer, tau16 + acur resident, double-buffered (A row, AT row) stages.
@@ -141,10 +154,61 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       if (p.l2_prefetch >= 32 / m) p.l2_prefetch = 32 / m - 1;
     }
   }
+  // Long rows of float storage: the quantized-filter kernel (scan_filter.cuh)
+  // reads int16 (or int8) copies of the rows and verifies the few surviving
+  // candidates exactly.  LSAPGPU_SCAN_FILTER=0 disables it, =2 forces it at
+  // any n (tests); LSAPGPU_FILTER_BITS=8|16, LSAPGPU_FILTER_RB=1|2 and
+  // LSAPGPU_FILTER_QUEUE=k pin the geometry so tests reach every path.
+  int filt = 1;
+  if (const char* f = std::getenv("LSAPGPU_SCAN_FILTER")) filt = std::atoi(f);
+  if (filt && d.storage == kF32 && d.n < 131072 && (!p.resident || filt >= 2) &&
+      !std::getenv("LSAPGPU_SCAN_BUDGET")) {
+    const size_t limit = 232448 - 8 * 1024;  // dynamic smem next to the kernel's static ~7 KB
+    int want_bits = 0, want_rb = 0;
+    if (const char* b = std::getenv("LSAPGPU_FILTER_BITS")) want_bits = std::atoi(b);
+    if (const char* r = std::getenv("LSAPGPU_FILTER_RB")) want_rb = std::atoi(r);
+    int want_q = -1;
+    if (const char* qq = std::getenv("LSAPGPU_FILTER_QUEUE")) want_q = std::max(0, std::min(kFilterQueueMax, std::atoi(qq)));
+    // prefer int16 copies, double-buffered rows, >= 4 slots, a 1024-entry
+    // queue; shrink the queue (to 512) before giving up a row buffer
+    bool done = false;
+    for (int qb : {2, 1}) {
+      if (want_bits && want_bits != 8 * qb) continue;
+      for (int rb : {2, 1}) {
+        if (want_rb && want_rb != rb) continue;
+        for (int qcap : {kFilterQueueMax, kFilterQueueMax / 2}) {
+          if (want_q >= 0) qcap = want_q;
+          int ns = 8;
+          while (ns >= 3 && filter_smem(d.ld, qb, rb, ns, qcap) > limit) --ns;
+          if (ns < 3) continue;
+          p.filter = 8 * qb;
+          p.m = rb;
+          p.bufs = ns;
+          p.resident = 0;
+          p.passes = 1;
+          p.chunk = kFilterChunk;
+          p.threads = 32 * 19;
+          p.smem = filter_smem(d.ld, qb, rb, ns, qcap);
+          p.ctas = num_sms;
+          p.max_segments = 1;
+          p.l2_prefetch = 0;
+          p.filter_queue = qcap;
+          done = true;
+          break;
+        }
+        if (done) break;
+      }
+      if (done) break;
+    }
+  }
   return p;
 }
 
 cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  if (p.filter) {
+    if (d.storage != kF32 || !d.Q || !d.QT || !d.aux) return cudaErrorInvalidValue;
+    return launch_scan_filter_typed<float>(d, p, full, st);
+  }
   if (p.resident) {
     switch (d.storage) {
       case kI16:

@@ -1,0 +1,458 @@
+#pragma once
+// scan_filter.cuh -- the pair scan for long rows (n beyond what the resident
+// kernel holds on chip: C4 n = 30000, C5 n = 100000), computing the same
+// records as every other scan kernel (kernels_scalar.cpp:6-25,
+// kernels_avx2.cpp:40-92, solver_state.hpp:78-104) with a quantized filter
+// and an exact verification step.
+//
+// Work item: agent i with its job j0 = tau[i]; over every position p with
+// t = tau[p], g = A[i][t], x = AT[j0][p], c = acur[p], s = acur[i]:
+//   agent candidate (g - s) + (x - c), tie index t
+//   job   candidate (x - s) + (g - c), tie index p
+// in fp64, maximum with the smallest index on ties, active iff > eps.
+//
+// Filter.  Both candidates are roundings of the same real D = g + x - c - s.
+// With a power-of-two scale S (max |a| * S <= 16383 for 16-bit, 127 for
+// 8-bit) the layout keeps Q = ceil(A * S) and QT = ceil(AT * S), and the
+// per-launch position array aux[p] = tau[p] sizeof(Q) | (floor(acur[p] * S) + 2^14) << 17.
+// U = Q[i][t] + QT[j0][p] - floor(c * S) is an integer with
+//   (g + x - c) S  <=  U  <  (g + x - c) S + 3.
+// A position can be discarded without changing either record when
+//   * U < floor((s + eps) S) - 1: then D < eps - 1/S, so neither candidate
+//     is active (the fp64 rounding of D is far below 1/S), or
+//   * U < U_r - 4 for another position r: then D_r - D_p > 2/S, so r beats p
+//     strictly on both sides (no tie either).
+// Everything else goes to a per-item queue and is evaluated EXACTLY (fp64,
+// the reference's operation order) from the fp32 A / AT / acur in HBM, so
+// the records are bit-identical to the unfiltered scans'.  On uniform data
+// a few dozen of n positions survive per item; a queue overflow (adversarial
+// ties) falls back to an exact scan of the whole item.
+//
+// Data movement per item: the Q row (gathered at random t: staged in shared
+// memory by TMA) and the QT row (streamed through a ring of TMA chunk slots)
+// -- 2 n sizeof(Q) bytes of HBM instead of 2 n sizeof(float) -- plus aux[]
+// (4 n bytes, L2-resident, shared by every item of the launch), which the
+// consumers load straight into registers (through shared memory it cost as
+// much smem bandwidth as the gather).  Row buffers are double-buffered where
+// two fit.
+//
+// Warps: 16 consumers (each takes one 256-position block of every chunk),
+// one row producer, one chunk producer, one verifier that evaluates item q's
+// queue while the consumers scan item q + 1.
+#include "scan_resident.cuh"
+
+namespace lsapgpu {
+namespace scan_detail {
+
+constexpr int kFW = 16;                     // consumer warps
+constexpr int kFV = 8;                      // positions per lane per block
+constexpr int kFBlk = 32 * kFV;             // 256 positions per warp block
+constexpr int32_t kFChunk = kFW * kFBlk;    // 4096 positions per chunk (one block per consumer warp)
+constexpr int kFThreads = 32 * (kFW + 3);   // + row producer, chunk producer, verifier
+constexpr int kFQueueMax = 1024;            // candidates per item (two item parities) at most
+constexpr int kFMaxSlots = 8;
+constexpr int kFEdgeBuf = 128;
+constexpr int32_t kAuxBias = 16384;         // bias of the 15-bit floor(c S) field
+constexpr int32_t kFNeg = -(1 << 24);       // below every U
+
+struct FInfo {
+  int32_t agent;
+  int32_t job;
+  uint32_t flags;
+  int32_t t0;  // eps gate in biased U units
+  double sv;   // acur[agent]
+};
+
+template <class Q>
+__device__ __forceinline__ int32_t q_elem(const uint4& w, int v) {
+  if constexpr (sizeof(Q) == 2) {
+    const uint32_t x = (&w.x)[v >> 1];
+    return (v & 1) ? (static_cast<int32_t>(x) >> 16) : static_cast<int32_t>(static_cast<int16_t>(x & 0xFFFFu));
+  } else {
+    const uint32_t x = (&w.x)[v >> 2];
+    return static_cast<int32_t>(x << (24 - 8 * (v & 3))) >> 24;
+  }
+}
+
+__device__ __forceinline__ int32_t eps_gate(double sv, double eps, double S) {
+  const double r = floor((sv + eps) * S);
+  if (!(r < 1e9)) return 1 << 24;  // (also NaN-safe) nothing can be active
+  if (r < -1e9) return kFNeg;
+  return static_cast<int32_t>(r) - 1 - kAuxBias;
+}
+
+// smem: rows [RB][ld] Q | slots [NS] x QT chunk [C] Q | queue [2][qcap] u64 |
+//       row_full[RB], slot_full[NS], slot_empty[NS], item_done[2], queue_free[2] mbarriers
+template <class E, class Q, int RB>
+__global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState st, int full, int NS, int qcap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int32_t n = st.n;
+  const int64_t ld = st.ld;
+  const Q* __restrict__ Qg = static_cast<const Q*>(st.Q);
+  const Q* __restrict__ QTg = static_cast<const Q*>(st.QT);
+  const uint32_t* __restrict__ aux_g = st.aux;
+  const E* __restrict__ A = static_cast<const E*>(st.A);
+  const E* __restrict__ AT = static_cast<const E*>(st.AT);
+  const E* __restrict__ acur_g = static_cast<const E*>(st.acur);
+  const int32_t* __restrict__ tau_g = st.tau;
+  const double S = st.qscale;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();
+  pdl_wait();  // the aux build (and the commit / apply before it) wrote what this scan reads
+  if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
+
+  const int32_t count = full ? n : (st.use_own ? st.ctrl->own_count : st.ctrl->work_count);
+  const uint32_t* __restrict__ items = st.use_own ? st.items_own : st.items;
+  const int32_t stages = count > static_cast<int32_t>(blockIdx.x)
+                             ? (count - static_cast<int32_t>(blockIdx.x) + gridDim.x - 1) / gridDim.x
+                             : 0;
+  if (stages == 0) return;
+  const int32_t nch = static_cast<int32_t>((n + kFChunk - 1) / kFChunk);
+  const int parity_out = st.ctrl->parity;
+
+  const size_t row_bytes = (static_cast<size_t>(ld) * sizeof(Q) + 127) / 128 * 128;
+  constexpr size_t kSlotBytes = static_cast<size_t>(kFChunk) * sizeof(Q);
+  Q* rows = reinterpret_cast<Q*>(smem_raw);
+  unsigned char* slots = smem_raw + RB * row_bytes;
+  unsigned long long* queue = reinterpret_cast<unsigned long long*>(slots + NS * kSlotBytes);  // [2][qcap]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(queue + 2 * qcap);
+  uint64_t* row_full = bars;
+  uint64_t* slot_full = bars + RB;
+  uint64_t* slot_empty = slot_full + kFMaxSlots;
+  uint64_t* item_done = slot_empty + kFMaxSlots;
+  uint64_t* queue_free = item_done + 2;
+  __shared__ FInfo info_s[RB];
+  __shared__ FInfo vinfo[4];  // the verifier's copy (item q in q & 3)
+  __shared__ int qn[2];
+  __shared__ int tmax[2];
+  __shared__ Prop ebuf[kFEdgeBuf];
+  __shared__ int ebuf_n;
+
+  if (tid == 0) {
+    for (int k = 0; k < RB; ++k) mbar_init(&row_full[k], 1);
+    for (int k = 0; k < NS; ++k) {
+      mbar_init(&slot_full[k], 1);
+      mbar_init(&slot_empty[k], kFW);
+    }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&item_done[k], kFW);
+      mbar_init(&queue_free[k], 1);
+      qn[k] = 0;
+      tmax[k] = kFNeg;
+    }
+    ebuf_n = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto item_of = [&](int32_t q) -> FInfo {
+    FInfo it;
+    const int32_t idx = static_cast<int32_t>(blockIdx.x) + q * static_cast<int32_t>(gridDim.x);
+    const uint32_t w = full ? (static_cast<uint32_t>(idx) | kItemAgent | kItemJob) : items[idx];
+    it.agent = static_cast<int32_t>(w & kItemMask);
+    it.job = tau_g[it.agent];
+    it.flags = w & (kItemAgent | kItemJob);
+    it.sv = static_cast<double>(acur_g[it.agent]);
+    it.t0 = eps_gate(it.sv, st.eps, S);
+    return it;
+  };
+
+  if (warp == kFW) {
+    // ---------------- row producer: Q[i,:] of item q into row buffer q % RB ----------------
+    // (8 KB pieces, one per lane: a lane issues its bulk copies one after another
+    // at ~0.2 us each, so several lanes keep a row's copies in flight together;
+    // B200 TMA from HBM: 3.1 TB/s issued from one lane, 6.8 TB/s from four)
+    FInfo nxt = item_of(0);
+    const uint32_t rbytes = static_cast<uint32_t>(ld * sizeof(Q));
+    constexpr uint32_t kPiece = 8192;
+    const int pieces = static_cast<int>((rbytes + kPiece - 1) / kPiece);
+    for (int32_t q = 0; q < stages; ++q) {
+      const FInfo cur = nxt;
+      const int rb = q % RB;
+      if (q >= RB) mbar_wait_backoff(&item_done[(q - RB) & 1], static_cast<uint32_t>(((q - RB) >> 1) & 1), 64);
+      if (lane == 0) {
+        info_s[rb] = cur;
+        vinfo[q & 3] = cur;
+        mbar_expect_tx(&row_full[rb], rbytes);
+      }
+      __syncwarp();
+      for (int pc = lane; pc < pieces; pc += 32) {
+        const uint32_t off = static_cast<uint32_t>(pc) * kPiece;
+        const uint32_t sz = (rbytes - off) < kPiece ? (rbytes - off) : kPiece;
+        bulk_g2s(reinterpret_cast<unsigned char*>(rows) + rb * row_bytes + off,
+                 reinterpret_cast<const unsigned char*>(Qg + static_cast<int64_t>(cur.agent) * ld) + off, sz,
+                 &row_full[rb]);
+      }
+      if (q + 1 < stages) nxt = item_of(q + 1);
+    }
+  } else if (warp == kFW + 1) {
+    // ---------------- chunk producer: QT chunk c of item q into the slot ring ----------------
+    int s = 0;
+    uint32_t eph = 0;   // parity of the slot_empty phase to wait for
+    bool wrapped = false;
+    int32_t job_next = item_of(0).job;
+    for (int32_t q = 0; q < stages; ++q) {
+      const int32_t job = job_next;
+      if (q + 1 < stages) job_next = item_of(q + 1).job;
+      for (int32_t c = 0; c < nch; ++c) {
+        if (wrapped) mbar_wait_backoff(&slot_empty[s], eph, 32);
+        const int64_t p0 = static_cast<int64_t>(c) * kFChunk;
+        const uint32_t len = static_cast<uint32_t>((ld - p0) < kFChunk ? (ld - p0) : kFChunk);
+        const uint32_t qbytes = len * static_cast<uint32_t>(sizeof(Q));
+        constexpr uint32_t kP = 4096;
+        const uint32_t nq = (qbytes + kP - 1) / kP;
+        if (lane == 0) mbar_expect_tx(&slot_full[s], qbytes);
+        __syncwarp();
+        if (static_cast<uint32_t>(lane) < nq) {
+          const uint32_t off = lane * kP;
+          bulk_g2s(slots + s * kSlotBytes + off,
+                   reinterpret_cast<const unsigned char*>(QTg + static_cast<int64_t>(job) * ld + p0) + off,
+                   min(kP, qbytes - off), &slot_full[s]);
+        }
+        __syncwarp();
+        if (++s == NS) {
+          s = 0;
+          if (wrapped) eph ^= 1u;
+          wrapped = true;
+        }
+      }
+    }
+  } else if (warp == kFW + 2) {
+    // ---------------- verifier: exact records of item q from its queue ----------------
+    long long kept = 0, overflows = 0;
+    for (int32_t q = 0; q < stages; ++q) {
+      const int par = q & 1;
+      mbar_wait_backoff(&item_done[par], static_cast<uint32_t>((q >> 1) & 1), 64);
+      const FInfo im = vinfo[q & 3];
+      const int cnt = qn[par];
+      kept += cnt;
+      const double s = im.sv;
+      const E* arow = A + static_cast<int64_t>(im.agent) * ld;
+      const E* xrow = AT + static_cast<int64_t>(im.job) * ld;
+      Track<kFloat> ta, tj;
+      ta.init();
+      tj.init();
+      if (cnt <= qcap) {
+        for (int e = lane; e < cnt; e += 32) {
+          const unsigned long long ent = queue[par * qcap + e];
+          const int32_t p = static_cast<int32_t>(ent & 0xFFFFFFFFull);
+          const int32_t t = static_cast<int32_t>(ent >> 32);
+          const double gv = static_cast<double>(arow[t]);
+          const double xv = static_cast<double>(xrow[p]);
+          const double cv = static_cast<double>(acur_g[p]);
+          ta.add(delta4(gv, s, xv, cv), t);
+          tj.add(delta4(xv, s, gv, cv), p);
+        }
+      } else {  // queue overflow (heavy ties): exact scan of the whole item
+        ++overflows;
+        for (int32_t p = lane; p < n; p += 32) {
+          const int32_t t = tau_g[p];
+          const double gv = static_cast<double>(arow[t]);
+          const double xv = static_cast<double>(xrow[p]);
+          const double cv = static_cast<double>(acur_g[p]);
+          ta.add(delta4(gv, s, xv, cv), t);
+          tj.add(delta4(xv, s, gv, cv), p);
+        }
+      }
+      ta.warp_reduce();
+      tj.warp_reduce();
+      __syncwarp();
+      if (lane == 0) {
+        qn[par] = 0;
+        tmax[par] = kFNeg;
+        mbar_arrive(&queue_free[par]);
+      }
+      // records + proposals (entries filled in at the flush: finish_prop pad 2)
+      bool emit = false;
+      Prop entry;
+      if (lane < 2) {
+        const Track<kFloat>& r = lane == 0 ? ta : tj;
+        const bool ok = r.valid();
+        const double d = ok ? r.delta() : 0.0;
+        const int32_t k = ok ? r.index() : -1;
+        const bool active = ok && d > st.eps;
+        if (lane == 0 && (im.flags & kItemAgent)) {
+          st.agent_delta[im.agent] = active ? d : 0.0;
+          st.agent_partner[im.agent] = active ? k : -1;
+          emit = active && st.emit_edges;
+          if (emit) entry = Prop{im.agent, im.agent, -1, k, im.job, 2, d, 0.0, 0.0};
+        } else if (lane == 1 && (im.flags & kItemJob)) {
+          st.job_delta[im.job] = active ? d : 0.0;
+          st.job_partner[im.job] = active ? k : -1;
+          emit = active && st.emit_edges;
+          if (emit) entry = Prop{n + im.job, k, im.agent, im.job, -1, 2, d, 0.0, 0.0};
+        }
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, emit);
+      if (mask) {
+        const int base = ebuf_n;  // this warp is the only writer
+        if (emit) {
+          const int pos = base + __popc(mask & ((1u << lane) - 1));
+          if (pos < kFEdgeBuf) {
+            ebuf[pos] = entry;
+          } else {
+            const int gg = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
+            st.edges[parity_out][gg] = finish_prop(entry, st.sigma, tau_g, st.A, st.storage, ld, n);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ebuf_n = base + __popc(mask);
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {  // instrumentation: candidates verified, whole-item fallbacks
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st.ctrl->filter_kept), static_cast<unsigned long long>(kept));
+      if (overflows)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st.ctrl->filter_overflows),
+                  static_cast<unsigned long long>(overflows));
+    }
+  } else {
+    // ---------------- consumers: block `warp` of every chunk ----------------
+    // The 8 aux words of a lane's positions come straight from L2 (aux is
+    // the same for every item of the launch), one chunk ahead in registers;
+    // only the QT chunk and the gathered Q row go through shared memory.
+    const int32_t lo = warp * kFBlk + lane * kFV;  // position offset within a chunk
+    int s = 0;
+    uint32_t fph = 0;  // slot_full phase parity
+    auto load_aux = [&](int32_t c, uint4& x0, uint4& x1) {
+      const int64_t p = static_cast<int64_t>(c) * kFChunk + lo;
+      if (p < n) {
+        x0 = __ldcg(reinterpret_cast<const uint4*>(aux_g + p));
+        x1 = __ldcg(reinterpret_cast<const uint4*>(aux_g + p + 4));
+      } else {
+        x0 = make_uint4(0u, 0u, 0u, 0u);
+        x1 = x0;
+      }
+    };
+    uint4 n0, n1;
+    load_aux(0, n0, n1);
+    for (int32_t q = 0; q < stages; ++q) {
+      const int rb = q % RB;
+      const int par = q & 1;
+      mbar_wait_backoff(&row_full[rb], static_cast<uint32_t>((q / RB) & 1), 32);
+      if (q >= 2) mbar_wait_backoff(&queue_free[par], static_cast<uint32_t>(((q - 2) >> 1) & 1), 32);
+      const int32_t t0 = info_s[rb].t0;
+      const unsigned char* rowb = reinterpret_cast<const unsigned char*>(rows) + static_cast<size_t>(rb) * row_bytes;
+      int32_t T = t0;
+      int32_t tshare = kFNeg;  // last read of tmax[par]
+      for (int32_t c = 0; c < nch; ++c) {
+        const uint4 a0 = n0, a1 = n1;
+        load_aux(c + 1 < nch ? c + 1 : 0, n0, n1);  // next chunk (or chunk 0 of the next item)
+        mbar_wait_backoff(&slot_full[s], fph, 20);
+        const unsigned char* sb = slots + s * kSlotBytes;
+        uint4 qv;
+        if constexpr (sizeof(Q) == 2) {
+          qv = *reinterpret_cast<const uint4*>(sb + lo * 2);
+        } else {
+          const uint2 h = *reinterpret_cast<const uint2*>(sb + lo);
+          qv = make_uint4(h.x, h.y, 0u, 0u);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_empty[s]);  // QT values live in registers now
+        if (++s == NS) {
+          s = 0;
+          fph ^= 1u;
+        }
+        const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const int32_t p0 = c * kFChunk + lo;
+        // aux low 17 bits = the BYTE offset of Q[i][t] in the staged row, so a
+        // gather is one LOP3 + one LDS [reg + uniform base]
+        int32_t U[kFV];
+#pragma unroll
+        for (int v = 0; v < kFV; ++v) {
+          const uint32_t off = aw[v] & 0x1FFFFu;
+          const int32_t cb = static_cast<int32_t>(aw[v] >> 17);
+          U[v] = static_cast<int32_t>(*reinterpret_cast<const Q*>(rowb + off)) + q_elem<Q>(qv, v) - cb;
+        }
+        if (c == nch - 1) {  // the ragged last chunk: positions past n (aux word 0) never count
+#pragma unroll
+          for (int v = 0; v < kFV; ++v) U[v] = (p0 + v < n) ? U[v] : kFNeg;
+        }
+        int32_t m = U[0];
+#pragma unroll
+        for (int v = 1; v < kFV; ++v) m = max(m, U[v]);
+        // the CTA's best bound, read (plain LDS) one chunk late: a stale,
+        // lower T only keeps more candidates, never drops one
+        T = max(T, tshare - 4);
+        // Common path: no lane reaches T (once an item's maximum is known,
+        // almost every block), one vote and nothing else.  A block that
+        // reaches T raises T to its own max - 4, tests its positions one by
+        // one and publishes the max for the other warps.
+        if (__any_sync(0xffffffffu, m >= T)) {
+          const int32_t wm = __reduce_max_sync(0xffffffffu, m);
+          T = max(T, wm - 4);
+          if (lane == 0) atomicMax(&tmax[par], wm);
+          uint32_t bits = 0;
+#pragma unroll
+          for (int v = 0; v < kFV; ++v) bits |= (U[v] >= T ? 1u : 0u) << v;
+          if (bits) {
+            int pos = atomicAdd(&qn[par], __popc(bits));
+#pragma unroll
+            for (int v = 0; v < kFV; ++v)
+              if ((bits >> v) & 1u) {
+                if (pos < qcap)
+                  queue[par * qcap + pos] = static_cast<unsigned long long>(static_cast<uint32_t>(p0 + v)) |
+                                            (static_cast<unsigned long long>((aw[v] & 0x1FFFFu) / sizeof(Q)) << 32);
+                ++pos;
+              }
+          }
+        }
+        tshare = *reinterpret_cast<volatile int*>(&tmax[par]);  // used at the next chunk
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&item_done[par]);  // releases row buffer rb and hands the queue over
+    }
+  }
+  __syncthreads();
+  const int ne = min(ebuf_n, kFEdgeBuf);
+  __shared__ int gbase;
+  if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
+  __syncthreads();
+  for (int e = tid; e < ne; e += kFThreads)
+    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.A, st.storage, ld, n);
+}
+
+// Per-launch position array: aux[p] = tau[p] * sizeof(Q) | (floor(acur[p] * S) + 2^14) << 17
+// (the byte offset of the gathered element in a staged Q row: < 2^17 for
+// every plan, int16 copies are only chosen when two rows fit on chip).
+template <class E, class Q>
+__global__ void filter_aux_kernel(DevState st) {
+  pdl_trigger();
+  pdl_wait();
+  const E* acur = static_cast<const E*>(st.acur);
+  const double S = st.qscale;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < st.ld;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t w = 0;
+    if (p < st.n) {
+      const int32_t cq = static_cast<int32_t>(floor(static_cast<double>(acur[p]) * S)) + kAuxBias;
+      w = static_cast<uint32_t>(st.tau[p]) * static_cast<uint32_t>(sizeof(Q)) | (static_cast<uint32_t>(cq) << 17);
+    }
+    st.aux[p] = w;
+  }
+}
+
+template <class E, class Q, int RB>
+cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  cudaError_t e = launch_pdl(filter_aux_kernel<E, Q>, dim3(p.ctas), dim3(256), 0, st, d.pdl, d);
+  if (e != cudaSuccess) return e;
+  auto k = pair_scan_filter_kernel<E, Q, RB>;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k, dim3(p.ctas), dim3(kFThreads), p.smem, st, d.pdl, d, full, p.bufs, p.filter_queue);
+}
+
+}  // namespace scan_detail
+
+template <class E>
+cudaError_t launch_scan_filter_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  if (p.filter == 16)
+    return p.m == 2 ? scan_detail::launch_filter_t<E, int16_t, 2>(d, p, full, st)
+                    : scan_detail::launch_filter_t<E, int16_t, 1>(d, p, full, st);
+  return p.m == 2 ? scan_detail::launch_filter_t<E, int8_t, 2>(d, p, full, st)
+                  : scan_detail::launch_filter_t<E, int8_t, 1>(d, p, full, st);
+}
+
+}  // namespace lsapgpu

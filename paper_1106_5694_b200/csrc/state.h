@@ -25,6 +25,13 @@ struct DevState {
   int32_t* tau = nullptr;    // agent -> job (padded to ld)
   uint16_t* tau16 = nullptr; // the same as uint16 when n < 65536 (the resident scan bulk-loads it)
   void* acur = nullptr;      // A[i][tau[i]] (storage type, padded to ld)
+  // quantized filter copies for the long-row scan (scan_filter.cuh), pitch ld:
+  // Q = ceil(A * qscale), QT = ceil(AT * qscale) as int16 or int8, and the
+  // per-launch position array aux[p] = tau[p] | (floor(acur[p] * qscale) + 2^14) << 17
+  const void* Q = nullptr;
+  const void* QT = nullptr;
+  uint32_t* aux = nullptr;
+  double qscale = 0.0;
 
   double* agent_delta = nullptr;
   int32_t* agent_partner = nullptr;
@@ -102,8 +109,12 @@ cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, 
                                 int storage, void* A, void* AT, int64_t ld, cudaStream_t st);
 cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaStream_t st);
 // classify + build in one pass for a speculated storage type (flags as launch_classify)
+// amax (nullable): atomicMax of the float bits of every |entry| rounded up (the filter's scale)
 cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
-                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st);
+                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st,
+                                uint32_t* amax = nullptr);
+// Q = ceil(A * scale), QT = ceil(AT * scale) as int16 (qbits 16) or int8 (qbits 8), padding zeroed
+cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st);
 cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st);  // tau, acur from sigma
 // out[j] = A[sigma[j]][j] (fp64); pack: also sigma and tau as int32 after it (2n doubles)
 cudaError_t launch_gather_current(const DevState& d, double* out, cudaStream_t st, int pack = 0);
@@ -123,10 +134,15 @@ struct ScanPlan {
   int resident = 0;     // 1: resident-state kernel (scan_resident.cuh)
   int depth = 2;        // streaming kernel: vector steps of the streamed rows in flight
   int l2_prefetch = 0;  // resident kernel: stages whose rows are prefetched into L2 ahead
+  int filter = 0;       // 8 / 16: quantized-filter kernel (scan_filter.cuh) with int8 / int16 copies;
+                        // m = row buffers, bufs = chunk slots
+  int filter_queue = 1024;  // filter kernel: candidates per item before the exact whole-item fallback
+  int launches() const { return filter ? 2 : 1; }  // kernels per scan (the filter adds the aux build)
   bool operator==(const ScanPlan& o) const {
     return m == o.m && passes == o.passes && chunk == o.chunk && bufs == o.bufs && ctas == o.ctas &&
            threads == o.threads && smem == o.smem && max_segments == o.max_segments && resident == o.resident &&
-           depth == o.depth && l2_prefetch == o.l2_prefetch;
+           depth == o.depth && l2_prefetch == o.l2_prefetch && filter == o.filter &&
+           filter_queue == o.filter_queue;
   }
 };
 ScanPlan plan_scan(const DevState& d, int num_sms);

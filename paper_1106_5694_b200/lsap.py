@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 from typing import List, Optional, Tuple
 
@@ -202,10 +203,52 @@ class AppliedExchange:
     delta: float = 0.0
 
 
+class ObjectiveTrace(Sequence):
+    """SolveReport::objective_trace (types.hpp:97-105): (switches, value)
+    pairs, held as the two arrays the library filled and turned into Python
+    tuples only when read (a 10^5-entry trace is ~10 ms of tuple building)."""
+
+    __slots__ = ("switches", "values")
+
+    def __init__(self, switches: np.ndarray, values: np.ndarray):
+        self.switches = switches
+        self.values = values
+
+    def __len__(self) -> int:
+        return len(self.switches)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return list(zip(self.switches[k].tolist(), self.values[k].tolist()))
+        return (int(self.switches[k]), float(self.values[k]))
+
+    def __iter__(self):
+        return iter(zip(self.switches.tolist(), self.values.tolist()))
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, ObjectiveTrace):
+            return (np.array_equal(self.switches, other.switches)
+                    and np.array_equal(self.values, other.values))
+        try:
+            other = list(other)
+        except TypeError:
+            return NotImplemented
+        if len(other) != len(self):
+            return False
+        if not other:
+            return True
+        sw = np.array([t[0] for t in other], np.int64)
+        va = np.array([t[1] for t in other], np.float64)
+        return np.array_equal(self.switches, sw) and np.array_equal(self.values, va)
+
+    def __repr__(self) -> str:
+        return f"ObjectiveTrace({len(self)} entries)"
+
+
 @dataclass
 class SolveReport:
     assignment: Assignment
-    objective_trace: List[Tuple[int, float]] = field(default_factory=list)
+    objective_trace: Sequence[Tuple[int, float]] = field(default_factory=list)
     outer_iterations: int = 0
     switches_applied: int = 0
     elapsed: int = 0  # nanoseconds
@@ -409,7 +452,7 @@ class Context:
         k = min(tl.value, cap)
         rep = SolveReport(
             assignment=Assignment(sigma, tau, st.value),
-            objective_trace=list(zip(ts[:k].tolist(), tv[:k].tolist())) if trace else [],
+            objective_trace=ObjectiveTrace(ts[:k], tv[:k]) if trace else [],
             outer_iterations=st.outer_iterations,
             switches_applied=st.switches_applied,
             elapsed=int(st.elapsed_ms * 1e6),
@@ -557,6 +600,17 @@ class Context:
                                               C.byref(cm), C.byref(cl)))
         return {"scan_ms": tot.value, "scan_launches": la.value, "full_ms": fl.value,
                 "full_launches": fla.value, "commit_ms": cm.value, "commit_launches": cl.value}
+
+    def scan_plan(self) -> dict:
+        """The pair-scan plan chosen for the current matrix (lsapgpu_scan_plan)."""
+        info = np.zeros(16, np.int32)
+        k = N.LIB.lsapgpu_scan_plan(self.h, N.ptr(info), 16)
+        if k < 0:
+            self._check(k)
+        names = ["kernel", "m", "bufs", "filter", "ctas", "threads", "smem", "chunk", "filter_queue"]
+        out = dict(zip(names, info[:k].tolist()))
+        out["kernel"] = ["streaming", "resident", "filter"][out["kernel"]]
+        return out
 
 
 _ctx_lock = threading.Lock()

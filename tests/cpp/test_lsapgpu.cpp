@@ -19,9 +19,15 @@
 #include "lsap/core.hpp"
 #include "lsap/dgs.hpp"
 #include "lsap/geom.hpp"
+#include "lsap/kernels.hpp"
 #include "lsap/parallel.hpp"
 #include "lsap/rng.hpp"
 #include "lsapgpu.hpp"
+#include "lsapgpu_engine.hpp"
+
+#include <map>
+#include <sstream>
+#include <tuple>
 
 using namespace lsap;
 
@@ -226,6 +232,75 @@ int main() {
       try { auction_solve(g256, bad); } catch (const Error& e) { ref_msg = e.what(); }
       try { gpu::auction_solve(g256, bad); } catch (const Error& e) { gpu_msg = e.what(); }
       CHECK(!ref_msg.empty() && ref_msg == gpu_msg);
+    }
+    {  // engine plumbing (bench.cpp:77-96,210-253,281-396; lsap_bench.cpp:172-186)
+      const EngineSpec sp = gpu::parse_engine_spec(" dgs-gpu:eps=0.5:reeval=touched ");
+      CHECK(sp.name == "dgs-gpu" && sp.display == "dgs-gpu:eps=0.5:reeval=touched");
+      CHECK(sp.params.at("eps") == "0.5" && sp.params.at("reeval") == "touched");
+      CHECK(gpu::parse_engine_spec("dgs-par:workers=2").name == "dgs-par");
+      std::string m1, m2;
+      try { gpu::parse_engine_spec("dgs-warp"); } catch (const Error& e) { m1 = e.what(); }
+      try { parse_engine_spec("dgs-warp"); } catch (const Error& e) { m2 = e.what(); }
+      CHECK(!m1.empty() && m1 == m2);
+      m1.clear();
+      try { gpu::parse_engine_spec("dgs-gpu:eps"); } catch (const Error& e) { m1 = e.what(); }
+      CHECK(m1 == "bad engine parameter 'eps' in 'dgs-gpu:eps'");
+      m1.clear();
+      try {
+        gpu::run_engine(gpu::parse_engine_spec("dgs-gpu:reeval=sometimes"), generate_geom({16, 100.0, 1}), 0, {});
+      } catch (const Error& e) { m1 = e.what(); }
+      CHECK(m1 == "unknown reeval policy 'sometimes'");
+      // campaign cells: every GPU engine row equals its CPU engine's row
+      CampaignSpec cs;
+      cs.sizes = {48, 300};
+      cs.instances_per_size = 2;
+      cs.repetitions = 2;
+      cs.base_seed = 7;
+      for (const char* e : {"dgs-par", "dgs-gpu", "dgs-par:reeval=touched:eps=0.01", "dgs-gpu:reeval=touched:eps=0.01",
+                            "auction", "auction-gpu", "auction:scaling=1", "auction-gpu:scaling=1", "dgs-seq"})
+        cs.engines.push_back(gpu::parse_engine_spec(e));
+      cs.parallel_cells = 3;
+      std::ostringstream csv, summary;
+      CHECK(gpu::run_campaign(cs, csv, summary));
+      std::istringstream in(csv.str());
+      std::string line;
+      std::getline(in, line);
+      CHECK(line == csv_header());
+      std::map<std::tuple<std::string, std::int32_t, std::uint64_t, std::uint64_t>, BenchRecord> rows;
+      int nrows = 0;
+      while (std::getline(in, line)) {
+        const BenchRecord r = parse_csv_row(line);
+        rows[{r.engine, r.n, r.instance_seed, r.run_seed}] = r;
+        ++nrows;
+      }
+      CHECK(nrows == 2 * 2 * 2 * 9);
+      int pairs = 0;
+      for (const auto& [key, r] : rows) {
+        const std::string& eng = std::get<0>(key);
+        const auto pos = eng.find("-gpu");
+        if (pos == std::string::npos) continue;
+        const std::string cpu = eng.substr(0, pos) + (eng.substr(0, pos) == "dgs" ? "-par" : "") + eng.substr(pos + 4);
+        const auto it = rows.find({cpu, std::get<1>(key), std::get<2>(key), std::get<3>(key)});
+        CHECK(it != rows.end());
+        if (it == rows.end()) continue;
+        CHECK(r.objective == it->second.objective);
+        CHECK(r.iterations == it->second.iterations);
+        CHECK(r.terminated_by == it->second.terminated_by && r.terminated_by == "converged");
+        ++pairs;
+      }
+      CHECK(pairs == 4 * 2 * 2 * 2);
+      CHECK(summary.str().find("dgs-gpu") != std::string::npos);
+      // the solve command's JSON record: the "kernel" field
+      const Instance gi = generate_geom({300, 100.0, 3});
+      const EngineSpec dg = gpu::parse_engine_spec("dgs-gpu"), dp = gpu::parse_engine_spec("dgs-par");
+      const auto rg = gpu::run_engine(dg, gi, 5, {});
+      const auto rp = gpu::run_engine(dp, gi, 5, {});
+      CHECK(rg.assignment.sigma == rp.assignment.sigma);
+      const std::string jg = gpu::solve_record_json(dg, gi, rg), jp = gpu::solve_record_json(dp, gi, rp);
+      CHECK(jg.find("\"kernel\":\"sm_100a:") != std::string::npos);
+      CHECK(jp.find(std::string("\"kernel\":\"") + kernels::active().name + "\"") != std::string::npos);
+      CHECK(jg.find("\"engine\":\"dgs-gpu\"") != std::string::npos && jg.find("\"n\":300") != std::string::npos);
+      std::printf("engine record: %s\n", jg.c_str());
     }
   } catch (const std::exception& e) {
     std::fprintf(stderr, "exception: %s\n", e.what());

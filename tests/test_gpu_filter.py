@@ -1,0 +1,80 @@
+"""GPU: the quantized-filter long-row scan (csrc/scan_filter.cuh) is bit-exact.
+
+The kernel discards positions whose int16 / int8 upper bound cannot reach the
+eps gate or the item's best lower bound, and evaluates the rest exactly; its
+records must equal the unfiltered scan's (the oracle's, which restates
+kernels_scalar.cpp:6-25 / solver_state.hpp:78-104) bit for bit, on any fp32
+matrix: uniform, negative, huge / tiny magnitudes (extreme scales), heavy ties
+(queue overflow -> whole-item exact fallback), eps > 0, several chunks with
+a ragged tail.  The plan is read when the matrix is set, so each geometry
+runs in a fresh process with the environment pinning it."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = r'''
+import sys, numpy as np; sys.path.insert(0, %r)
+import paper_1106_5694_b200 as g
+from oracle.oracle import Oracle
+o = Oracle(); ctx = g.Context(0)
+rng = np.random.default_rng(7)
+
+def f32(x):
+    return np.asarray(x, np.float32).astype(np.float64)
+
+mats = [
+    ("unit", o.generate("f32", 1000, 11)),
+    ("unit-5000", o.generate("f32", 5000, 12)),            # two chunks, ragged tail
+    ("neg", f32(rng.uniform(-3.0, 1.0, (2100, 2100)))),
+    ("huge", f32(rng.uniform(-1.0, 1.0, (900, 900)) * 3e37)),
+    ("tiny", f32(rng.uniform(0.0, 1.0, (900, 900)) * 1e-36)),
+    ("ties", f32(rng.integers(0, 4, (1500, 1500)) * 0.375 + 0.1)),
+    ("spiky", f32(np.where(rng.random((1200, 1200)) < 0.01, 1e6, rng.random((1200, 1200))))),
+]
+for name, a in mats:
+    n = a.shape[0]
+    ctx.set_matrix(a)
+    assert ctx.scan_plan()["filter"] in (8, 16), (name, ctx.scan_plan())
+    for eps in (0.0, 1e-3):
+        s = o.random_perm(n, 4)
+        t = ctx.evaluate_all(s, eps)
+        ad, ap, jd, jp = o.evaluate_all(a, s, eps)
+        assert np.array_equal(t.agent_partner, ap) and np.array_equal(t.job_partner, jp), (name, eps)
+        assert np.array_equal(t.agent_delta.view(np.uint64), ad.view(np.uint64)), (name, eps)
+        assert np.array_equal(t.job_delta.view(np.uint64), jd.view(np.uint64)), (name, eps)
+    if n <= 2100:
+        for pi, policy in enumerate(("touched_and_conflicted", "touched_only")):
+            r = ctx.solve(g.ParallelConfig(seed=2, reeval=policy))
+            q = o.dgs_parallel(a, seed=2, policy=pi)
+            assert np.array_equal(r.assignment.sigma, q.sigma), (name, policy)
+            assert r.assignment.value == q.value and r.objective_trace == q.trace, (name, policy)
+            assert r.outer_iterations == q.outer_iterations, (name, policy)
+print("ok")
+''' % ROOT
+
+
+@pytest.mark.parametrize("env", [
+    {"LSAPGPU_SCAN_FILTER": "2"},                                                   # default geometry
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8"},                       # int8 copies
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "16", "LSAPGPU_FILTER_RB": "1"},  # single row buffer
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_RB": "1"},
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "0"},                      # every item: exact fallback
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "3"},                      # frequent overflow
+])
+def test_filter_scan_bit_exact(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", CASES], env=e, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_filter_is_the_default_long_row_scan(gpu_ctx):
+    """fp32 rows too long for the resident kernel take the filter kernel."""
+    gpu_ctx.generate("f32", 12000, 1)
+    plan = gpu_ctx.scan_plan()
+    assert plan["filter"] == 16 and plan["m"] == 2, plan

@@ -1,0 +1,5 @@
+O=gpurun_out/r2f; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_filter.py tests/test_gpu_golden.py -x -q > $O/pytest_filter.log 2>&1; echo "rc=$?" >> $O/pytest_filter.log
+timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_scan -s 0 -c 1 -o $O/filter_c4_full python tools/profile_target.py --kind f32 --n 30000 --stepped > $O/ncu_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_scan -s 0 -c 1 -o $O/filter_c5_full python tools/profile_target.py --kind f32 --n 100000 --stepped > $O/ncu_c5.log 2>&1
