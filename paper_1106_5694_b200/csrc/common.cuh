@@ -113,6 +113,12 @@ struct Ctrl {
   // quantized-filter scan (instrumentation): candidates verified exactly,
   // items that overflowed their queue (whole-item exact fallback)
   int64_t filter_kept, filter_overflows;
+  // filter scan self-check (DevState::filter_check): mismatches of the
+  // filtered records against an unfiltered scan of the same item, first one
+  int32_t fchk_mismatch, fchk_item, fchk_cnt, fchk_side;
+  int32_t fchk_want_k, fchk_got_k;
+  int32_t fchk_p, fchk_aux_ok, fchk_u, fchk_t0, fchk_tmax, fchk_pad;
+  double fchk_want_d, fchk_got_d;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <set>
 #include <string>
 #include <type_traits>
 #include <thread>
@@ -161,6 +162,7 @@ struct lsapgpu_ctx {
   std::vector<Buf> vec_bufs;
   Buf mat;                // A and AT (one allocation)
   Buf qmat;               // Q and QT: quantized filter copies (scan_filter.cuh), when the plan uses them
+  std::set<const void*> peer_poisoned;  // peer-transport flag arrays whose epochs a failed solve desynchronised
   Ctrl* ctrl_dev = nullptr;
   Ctrl* ctrl_host = nullptr;  // pinned mirror
   uint32_t* flags_dev = nullptr;
@@ -959,6 +961,7 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   ctx->d.pdl = 1;  // programmatic dependent launch for the inner-loop kernels (LSAPGPU_PDL=0: off)
   if (const char* e = std::getenv("LSAPGPU_PDL")) ctx->d.pdl = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSAPGPU_FILTER_CHECK")) ctx->d.filter_check = std::max(0, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||
@@ -1409,17 +1412,19 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     ps.world = dist->world;
     ps.rank = dist->rank;
     ps.bytes_per_rank = xbytes;
-    // the round epoch continues from the highest flag any rank has raised in
-    // this rank's buffer: every push raises its flag in every replica, so all
-    // ranks start from the same epoch, above anything already written -- also
-    // after a solve that one rank left early with an error (no stale buffer
-    // can then pass a wait)
-    uint64_t fl[kMaxPeers] = {};
-    CK(cudaMemcpyAsync(fl, dist->peer_flags[dist->rank], sizeof(uint64_t) * dist->world, cudaMemcpyDeviceToHost,
+    // the round epoch continues from this rank's own flag (its last push):
+    // ranks that finished the previous solve on these buffers agree on it.
+    // (Not the highest flag: a faster peer may already have pushed the first
+    // round of this solve.)  A solve that ended on a transport error leaves
+    // the epochs out of step, so the buffers are refused until the caller
+    // builds a fresh exchange (zeroed flags) on every rank.
+    if (ctx->peer_poisoned.count(dist->peer_flags[dist->rank]))
+      return fail(ctx, LSAPGPU_ERR_STATE,
+                  "peer exchange: a previous solve on these buffers failed; create a new exchange on every rank");
+    uint64_t e = 0;
+    CK(cudaMemcpyAsync(&e, dist->peer_flags[dist->rank] + dist->rank, sizeof(e), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    uint64_t e = 0;
-    for (int r = 0; r < dist->world; ++r) e = std::max(e, fl[r]);
     CK(cudaMemcpyAsync(&ctx->ctrl_dev->p2p_epoch, &e, sizeof(e), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
@@ -1630,7 +1635,10 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         const int code = C.error;
         C.error = 0;
         push_ctrl(ctx);
-        if (code == 2) return fail(ctx, LSAPGPU_ERR_CUDA, "peer exchange: a rank's records did not arrive (timeout)");
+        if (code == 2) {
+          if (p2p) ctx->peer_poisoned.insert(dist->peer_flags[dist->rank]);
+          return fail(ctx, LSAPGPU_ERR_CUDA, "peer exchange: a rank's records did not arrive (timeout)");
+        }
         return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
       }
       const int64_t cnt = C.log_count;
@@ -1721,6 +1729,19 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.scan_filter = ctx->scan_plan.filter;
   S.filter_kept = C.filter_kept - base.filter_kept;
   S.filter_overflows = C.filter_overflows - base.filter_overflows;
+  if (C.fchk_mismatch) {  // LSAPGPU_FILTER_CHECK diagnostics
+    char msg[256];
+    std::snprintf(msg, sizeof msg,
+                  "filter check: %d mismatching records; first %s %d (queue %d): want (%.17g, %d) got (%.17g, %d); "
+                  "wanted position %d aux_ok %d U %d t0 %d tmax %d",
+                  C.fchk_mismatch, C.fchk_side ? "job" : "agent", C.fchk_item, C.fchk_cnt, C.fchk_want_d,
+                  C.fchk_want_k, C.fchk_got_d, C.fchk_got_k, C.fchk_p, C.fchk_aux_ok, C.fchk_u, C.fchk_t0,
+                  C.fchk_tmax);
+    Ctrl& Cm = *ctx->ctrl_host;
+    Cm.fchk_mismatch = 0;
+    push_ctrl(ctx);
+    return fail(ctx, LSAPGPU_ERR_INTERNAL, msg);
+  }
   S.switches_applied = switches;
   const bool graphed = P.use_graph && (!multi || dist_graph);
   S.scan_launches = graphed ? S.outer_iterations + S.inner_iterations + graph_launches : launches;

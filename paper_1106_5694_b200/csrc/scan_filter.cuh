@@ -74,6 +74,16 @@ __device__ __forceinline__ int32_t q_elem(const uint4& w, int v) {
   }
 }
 
+// mbarrier arrive that cannot be issued before `dep` is computed (the value
+// is an asm operand): used to release a buffer only after loads from it have
+// been consumed.
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, uint32_t dep) {
+  asm volatile(
+      "{\n .reg .b32 d;\n mov.b32 d, %1;\n mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(smem_u32(bar)),
+      "r"(dep)
+      : "memory");
+}
+
 __device__ __forceinline__ int32_t eps_gate(double sv, double eps, double S) {
   const double r = floor((sv + eps) * S);
   if (!(r < 1e9)) return 1 << 24;  // (also NaN-safe) nothing can be active
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       mbar_init(&slot_empty[k], kFW);
     }
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&item_done[k], kFW);
+      mbar_init(&item_done[k], kFW * 32);  // every consumer lane arrives (its own queue stores released)
       mbar_init(&queue_free[k], 1);
       qn[k] = 0;
       tmax[k] = kFNeg;
@@ -258,11 +268,61 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       }
       ta.warp_reduce();
       tj.warp_reduce();
+      if (st.filter_check > 0 && (q % st.filter_check) == 0) {
+        // diagnostics: the same item unfiltered; any difference is recorded
+        Track<kFloat> ua, uj;
+        ua.init();
+        uj.init();
+        for (int32_t p = lane; p < n; p += 32) {
+          const int32_t t = tau_g[p];
+          const double gv = static_cast<double>(arow[t]);
+          const double xv = static_cast<double>(xrow[p]);
+          const double cv = static_cast<double>(acur_g[p]);
+          ua.add(delta4(gv, s, xv, cv), t);
+          uj.add(delta4(xv, s, gv, cv), p);
+        }
+        ua.warp_reduce();
+        uj.warp_reduce();
+        if (lane == 0) {
+          for (int side = 0; side < 2; ++side) {
+            const Track<kFloat>& w = side ? uj : ua;
+            const Track<kFloat>& f = side ? tj : ta;
+            const bool wa = w.valid() && w.delta() > st.eps, fa = f.valid() && f.delta() > st.eps;
+            const bool same = wa == fa && (!wa || (w.delta() == f.delta() && w.index() == f.index()));
+            if (!same && atomicAdd(&st.ctrl->fchk_mismatch, 1) == 0) {
+              st.ctrl->fchk_item = side ? im.job : im.agent;
+              st.ctrl->fchk_cnt = cnt;
+              st.ctrl->fchk_side = side;
+              st.ctrl->fchk_want_d = wa ? w.delta() : 0.0;
+              st.ctrl->fchk_want_k = wa ? w.index() : -1;
+              st.ctrl->fchk_got_d = fa ? f.delta() : 0.0;
+              st.ctrl->fchk_got_k = fa ? f.index() : -1;
+              // the wanted candidate's filter value from the copies in HBM,
+              // and what it was compared with
+              const int32_t wp = !wa ? -1 : (side ? w.index() : st.sigma[w.index()]);
+              if (wp >= 0) {
+                const int32_t wt = tau_g[wp];
+                const uint32_t a = aux_g[wp];
+                st.ctrl->fchk_p = wp;
+                st.ctrl->fchk_aux_ok = (a & 0x1FFFFu) == static_cast<uint32_t>(wt) * sizeof(Q) &&
+                                       static_cast<int32_t>(a >> 17) ==
+                                           static_cast<int32_t>(floor(static_cast<double>(acur_g[wp]) * S)) + kAuxBias;
+                st.ctrl->fchk_u = static_cast<int32_t>(Qg[static_cast<int64_t>(im.agent) * ld + wt]) +
+                                  static_cast<int32_t>(QTg[static_cast<int64_t>(im.job) * ld + wp]) -
+                                  static_cast<int32_t>(a >> 17);
+              }
+              st.ctrl->fchk_t0 = im.t0;
+              st.ctrl->fchk_tmax = tmax[par];
+            }
+          }
+        }
+      }
       __syncwarp();
       if (lane == 0) {
         qn[par] = 0;
         tmax[par] = kFNeg;
-        mbar_arrive(&queue_free[par]);
+        // (the reduced tracks depend on every lane's queue reads)
+        mbar_arrive_after(&queue_free[par], static_cast<uint32_t>(ta.i ^ tj.i));
       }
       // records + proposals (entries filled in at the flush: finish_prop pad 2)
       bool emit = false;
@@ -349,12 +409,6 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
           const uint2 h = *reinterpret_cast<const uint2*>(sb + lo);
           qv = make_uint4(h.x, h.y, 0u, 0u);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&slot_empty[s]);  // QT values live in registers now
-        if (++s == NS) {
-          s = 0;
-          fph ^= 1u;
-        }
         const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         const int32_t p0 = c * kFChunk + lo;
         // aux low 17 bits = the BYTE offset of Q[i][t] in the staged row, so a
@@ -380,7 +434,18 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
         // almost every block), one vote and nothing else.  A block that
         // reaches T raises T to its own max - 4, tests its positions one by
         // one and publishes the max for the other warps.
-        if (__any_sync(0xffffffffu, m >= T)) {
+        const bool hit = __any_sync(0xffffffffu, m >= T);
+        // Release the QT slot only after the vote: it consumed every lane's
+        // loads, and the arrive takes it as an operand, so no lane's LDS can
+        // still be in flight when the TMA refills the slot.  (An arrive right
+        // after the LDS did exactly that on a 3-slot ring: the self-check
+        // LSAPGPU_FILTER_CHECK caught dropped maxima at C5.)
+        if (lane == 0) mbar_arrive_after(&slot_empty[s], hit ? 1u : 0u);
+        if (++s == NS) {
+          s = 0;
+          fph ^= 1u;
+        }
+        if (hit) {
           const int32_t wm = __reduce_max_sync(0xffffffffu, m);
           T = max(T, wm - 4);
           if (lane == 0) atomicMax(&tmax[par], wm);
@@ -401,8 +466,9 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
         }
         tshare = *reinterpret_cast<volatile int*>(&tmax[par]);  // used at the next chunk
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&item_done[par]);  // releases row buffer rb and hands the queue over
+      // every lane arrives after its last use of row buffer rb and its own
+      // queue stores: releases the row and hands the queue to the verifier
+      mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
     }
   }
   __syncthreads();

@@ -32,6 +32,7 @@ struct DevState {
   const void* QT = nullptr;
   uint32_t* aux = nullptr;
   double qscale = 0.0;
+  int filter_check = 0;  // > 0: the filter scan re-verifies every k-th item unfiltered (diagnostics)
 
   double* agent_delta = nullptr;
   int32_t* agent_partner = nullptr;

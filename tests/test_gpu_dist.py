@@ -198,3 +198,34 @@ def test_peer_transport_two_processes_ipc(oracle, gpu_ctx, tmp_path):
     ref = gpu_ctx.solve(g.ParallelConfig(seed=6))
     for rank in range(2):
         assert np.array_equal(np.load(tmp_path / f"sigma{rank}.npy"), ref.assignment.sigma)
+
+
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_bench_two_ranks_sharded_block(tmp_path, exchange):
+    """bench.py at N = 2 (torchrun, gloo, both ranks on GPU 0): one JSON line
+    with the sharded C4 block of the metric's multi-GPU config -- the
+    sharded n = 30k solve must reproduce the reference's golden sigma
+    (tests/golden c4_f32_30000) and report its per-N sweep time and the
+    transport used."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = "29541" if exchange == "nccl" else "29542"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", port, os.path.join(root, "bench.py"),
+                        "--gpus", "2", "--backend", "gloo", "--exchange", exchange, "--steps", "2", "--warmup", "3",
+                        "--workload", "c1", "--blocks", "c4"],
+                       capture_output=True, text=True, timeout=1200, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["scaling"] == "strong"
+    blk = out["sharded"]["c4"]
+    assert "error" not in blk, blk
+    assert blk["n_gpus"] == 2 and blk["items_per_rank"] == 15000
+    assert blk["sigma_sha_matches_golden"] is True
+    assert blk["full_sweep_ms"] > 0 and blk["scan_kernel"] == "filter"
+    assert ("peer-memory" in blk["transport"]) == (exchange == "p2p")
