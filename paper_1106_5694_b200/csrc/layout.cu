@@ -99,12 +99,20 @@ __device__ __forceinline__ uint32_t entry_flags(double v) {
   return f;
 }
 
-__global__ void classify_kernel(Src src, int64_t row0, int64_t rows, uint32_t* flags) {
+__global__ void classify_kernel(Src src, int64_t row0, int64_t rows, uint32_t* flags, uint32_t* amax) {
   uint32_t f = 0;
+  float vmax = 0.f;
   const int64_t total = rows * src.n;  // flat over the block of rows: every thread busy
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    f |= entry_flags(src(row0 + e / src.n, static_cast<int32_t>(e % src.n)));
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = src(row0 + e / src.n, static_cast<int32_t>(e % src.n));
+    f |= entry_flags(v);
+    if (isfinite(v)) vmax = fmaxf(vmax, __double2float_ru(fabs(v)));
+  }
+  if (amax) {  // (per-thread atomics: the probe is 64 rows)
+    for (int off = 16; off > 0; off >>= 1) vmax = fmaxf(vmax, __shfl_down_sync(0xffffffffu, vmax, off));
+    if ((threadIdx.x & 31) == 0 && vmax > 0.f) atomicMax(amax, __float_as_uint(vmax));
+  }
   // warp then block OR, one atomic per block
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
   __shared__ uint32_t wf[32];
@@ -183,9 +191,32 @@ struct Pair<double> {
   __device__ static void st(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
 };
 
+// Quantized filter copies written by the layout pass itself (scan_filter.cuh):
+// element k of `Q` = ceil(v * scale) as int16 / int8 (exact: scale is a power
+// of two).  Two adjacent elements, the second only when `both`.
+__device__ __forceinline__ void qstore_pair(const QuantTarget& qt, int64_t k, double v0, double v1, bool both) {
+  const int32_t q0 = static_cast<int32_t>(ceil(v0 * qt.scale)), q1 = static_cast<int32_t>(ceil(v1 * qt.scale));
+  if (qt.bits == 16) {
+    int16_t* Q = static_cast<int16_t*>(qt.Q);
+    if (both)
+      *reinterpret_cast<uint32_t*>(Q + k) =
+          static_cast<uint16_t>(q0) | (static_cast<uint32_t>(static_cast<uint16_t>(q1)) << 16);
+    else
+      Q[k] = static_cast<int16_t>(q0);
+  } else {
+    int8_t* Q = static_cast<int8_t*>(qt.Q);
+    if (both)
+      *reinterpret_cast<uint16_t*>(Q + k) =
+          static_cast<uint16_t>(static_cast<uint8_t>(q0) | (static_cast<uint16_t>(static_cast<uint8_t>(q1)) << 8));
+    else
+      Q[k] = static_cast<int8_t>(q0);
+  }
+}
+
 template <class E>
 __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0, int64_t rows, E* A, E* AT,
-                                                           int64_t ld, uint32_t* flags, uint32_t* amax) {
+                                                           int64_t ld, uint32_t* flags, uint32_t* amax,
+                                                           QuantTarget qt) {
   __shared__ E tile[64][66];
   const int64_t bi = row0 + static_cast<int64_t>(blockIdx.y) * 64;  // agent block
   const int64_t bj = static_cast<int64_t>(blockIdx.x) * 64;         // job block
@@ -231,6 +262,7 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
       A[i * ld + j] = e0;
     tile[r][2 * lane] = e0;
     tile[r][2 * lane + 1] = e1;
+    if (qt.bits && j < n) qstore_pair(qt, i * ld + j, static_cast<double>(e0), static_cast<double>(e1), j + 1 < n);
   }
   __syncthreads();
   // AT rows bj .. bj+63, columns (agents) bi .. bi+63
@@ -243,6 +275,9 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
       Pair<E>::st(at, tile[2 * lane][c], tile[2 * lane + 1][c]);
     else if (ia < rend)
       at[0] = tile[2 * lane][c];
+    if (qt.bits && ia < rend)  // QT = the same values quantized, transposed
+      qstore_pair(QuantTarget{qt.QT, nullptr, qt.scale, qt.bits}, jj * ld + ia, static_cast<double>(tile[2 * lane][c]),
+                  static_cast<double>(tile[2 * lane + 1][c]), ia + 1 < rend);
   }
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
   __shared__ uint32_t wf[8];
@@ -356,9 +391,9 @@ struct BuildK {
 template <class E>
 struct FusedK {
   static void run(dim3 g, dim3 b, cudaStream_t st, Src s, int64_t r0, int64_t rows, void* A, void* AT,
-                  int64_t ld, uint32_t* flags, uint32_t* amax) {
+                  int64_t ld, uint32_t* flags, uint32_t* amax, QuantTarget qt) {
     layout_fused_kernel<E><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags,
-                                           amax);
+                                           amax, qt);
   }
 };
 template <class E>
@@ -401,13 +436,13 @@ cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaSt
 }
 
 cudaError_t launch_classify(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
-                            uint32_t* flags, cudaStream_t st) {
+                            uint32_t* flags, cudaStream_t st, uint32_t* amax) {
   Src src{s, n};
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  classify_kernel<<<sms * 8, 256, 0, st>>>(src, row0, rows, flags);
+  classify_kernel<<<sms * 8, 256, 0, st>>>(src, row0, rows, flags, amax);
   return cudaGetLastError();
 }
 
@@ -419,10 +454,11 @@ cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, 
 }
 
 cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
-                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st, uint32_t* amax) {
+                                void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st, uint32_t* amax,
+                                QuantTarget qt) {
   Src src{s, n};
   dim3 g(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
-  return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags, amax);
+  return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags, amax, qt);
 }
 
 cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st) {

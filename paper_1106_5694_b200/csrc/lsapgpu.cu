@@ -162,6 +162,9 @@ struct lsapgpu_ctx {
   std::vector<Buf> vec_bufs;
   Buf mat;                // A and AT (one allocation)
   Buf qmat;               // Q and QT: quantized filter copies (scan_filter.cuh), when the plan uses them
+  int quant_bits = 0;     // copies the last layout pass wrote (0: none) and their scale
+  double quant_scale = 0.0;
+  bool quant_fused = false;  // the current copies came from the layout pass (no quantize pass)
   std::set<const void*> peer_poisoned;  // peer-transport flag arrays whose epochs a failed solve desynchronised
   Ctrl* ctrl_dev = nullptr;
   Ctrl* ctrl_host = nullptr;  // pinned mirror
@@ -385,15 +388,8 @@ int alloc_matrix(lsapgpu_ctx* ctx, int32_t n, int storage) {
 // Quantized filter copies for the long-row scan (scan_filter.cuh): a
 // power-of-two scale with max|a| * scale <= 16383 (int16) or 127 (int8), from
 // the max the layout pass reduced into flags_dev[2], then Q / QT.
-int build_filter_copies(lsapgpu_ctx* ctx) {
-  DevState& d = ctx->d;
-  const ScanPlan& p = ctx->scan_plan;
-  uint32_t bits = 0;
-  CK(cpy(ctx, &bits, ctx->flags_dev + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  float amax = 0.f;
-  std::memcpy(&amax, &bits, sizeof(amax));
-  const double limit = p.filter == 16 ? 16383.0 : 127.0;
+double quant_scale_for(float amax, int bits) {
+  const double limit = bits == 16 ? 16383.0 : 127.0;
   double scale = 1.0;
   if (amax > 0.f) {
     int e = 0;
@@ -401,8 +397,12 @@ int build_filter_copies(lsapgpu_ctx* ctx) {
     scale = std::ldexp(1.0, std::max(-1000, std::min(1000, e - 1)));
     while (static_cast<double>(amax) * scale > limit) scale *= 0.5;
   }
-  const size_t qb = p.filter / 8;
-  const size_t bytes = static_cast<size_t>(d.n) * static_cast<size_t>(d.ld) * qb;
+  return scale;
+}
+
+int alloc_quant(lsapgpu_ctx* ctx, int bits, void** Q, void** QT) {
+  const DevState& d = ctx->d;
+  const size_t bytes = static_cast<size_t>(d.n) * static_cast<size_t>(d.ld) * static_cast<size_t>(bits / 8);
   if (ctx->qmat.bytes < 2 * bytes) {
     if (ctx->qmat.p) cudaFree(ctx->qmat.p);
     ctx->qmat.p = nullptr;
@@ -410,10 +410,69 @@ int build_filter_copies(lsapgpu_ctx* ctx) {
     CK(cudaMalloc(&ctx->qmat.p, 2 * bytes));
     ctx->qmat.bytes = 2 * bytes;
   }
-  d.Q = ctx->qmat.p;
-  d.QT = static_cast<unsigned char*>(ctx->qmat.p) + bytes;
+  *Q = ctx->qmat.p;
+  *QT = static_cast<unsigned char*>(ctx->qmat.p) + bytes;
+  return LSAPGPU_OK;
+}
+
+float bits_to_float(uint32_t b) {
+  float f = 0.f;
+  std::memcpy(&f, &b, sizeof(f));
+  return f;
+}
+
+// Before a layout pass of fp32 storage: if the scan plan for this matrix uses
+// the filter copies, size them and pick the scale from the probe rows' max
+// |a| so the layout pass writes Q / QT itself (no separate quantize pass);
+// finish_matrix checks the scale against the whole matrix's max afterwards.
+int prepare_quant(lsapgpu_ctx* ctx, int storage, float probe_amax, QuantTarget* qt) {
+  *qt = QuantTarget{};
+  ctx->quant_bits = 0;
+  if (storage != kF32) return LSAPGPU_OK;
+  DevState tmp = ctx->d;
+  tmp.storage = storage;
+  const ScanPlan p = plan_scan(tmp, ctx->num_sms);
+  if (!p.filter) return LSAPGPU_OK;
+  const int rc = alloc_quant(ctx, p.filter, &qt->Q, &qt->QT);
+  if (rc) return rc;
+  qt->scale = quant_scale_for(probe_amax, p.filter);
+  qt->bits = p.filter;
+  ctx->quant_bits = p.filter;
+  ctx->quant_scale = qt->scale;
+  return LSAPGPU_OK;
+}
+
+// Quantized filter copies for the long-row scan (scan_filter.cuh): a
+// power-of-two scale with max|a| * scale <= 16383 (int16) or 127 (int8), from
+// the max the layout pass reduced into flags_dev[2].  Normally the layout pass
+// already wrote them with the probe rows' scale; a separate pass runs only if
+// that scale does not hold for the whole matrix (or the layout was rebuilt).
+int build_filter_copies(lsapgpu_ctx* ctx) {
+  DevState& d = ctx->d;
+  const ScanPlan& p = ctx->scan_plan;
+  uint32_t bits = 0;
+  CK(cpy(ctx, &bits, ctx->flags_dev + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const float amax = bits_to_float(bits);
+  const double limit = p.filter == 16 ? 16383.0 : 127.0;
+  void *Q = nullptr, *QT = nullptr;
+  if (ctx->quant_bits == p.filter && static_cast<double>(amax) * ctx->quant_scale <= limit) {
+    const int rc = alloc_quant(ctx, p.filter, &Q, &QT);  // (already sized: same pointers)
+    if (rc) return rc;
+    d.Q = Q;
+    d.QT = QT;
+    d.qscale = ctx->quant_scale;
+    ctx->quant_fused = true;
+    return LSAPGPU_OK;
+  }
+  const double scale = quant_scale_for(amax, p.filter);
+  const int rc = alloc_quant(ctx, p.filter, &Q, &QT);
+  if (rc) return rc;
+  d.Q = Q;
+  d.QT = QT;
   d.qscale = scale;
-  CK(launch_quantize(d, p.filter, scale, const_cast<void*>(d.Q), const_cast<void*>(d.QT), ctx->stream));
+  ctx->quant_fused = false;
+  CK(launch_quantize(d, p.filter, scale, Q, QT, ctx->stream));
   ctx->launches += 2;
   return LSAPGPU_OK;
 }
@@ -445,25 +504,29 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   int rc = ensure_vectors(ctx, n);
   if (rc) return rc;
   ctx->n_matrix = 0;
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, 3 * sizeof(uint32_t), ctx->stream));
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, 4 * sizeof(uint32_t), ctx->stream));
   const int64_t probe = std::min<int64_t>(64, n);
-  CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream));
+  CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream, ctx->flags_dev + 3));
   ++ctx->launches;
-  uint32_t flags = 0;
-  CK(cpy(ctx, &flags, ctx->flags_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  uint32_t fl4[4] = {};
+  CK(cpy(ctx, fl4, ctx->flags_dev, sizeof(fl4), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  uint32_t flags = fl4[0];
   if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
   const int spec = storage_of_flags(flags);
   if ((rc = alloc_matrix(ctx, n, spec))) return rc;
   DevState& d = ctx->d;
+  QuantTarget qt;
+  if ((rc = prepare_quant(ctx, spec, bits_to_float(fl4[3]), &qt))) return rc;
   CK(launch_layout_fused(src, n, 0, n, spec, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
-                         ctx->flags_dev + 1, ctx->stream, ctx->flags_dev + 2));
+                         ctx->flags_dev + 1, ctx->stream, ctx->flags_dev + 2, qt));
   ++ctx->launches;
   CK(cpy(ctx, &flags, ctx->flags_dev + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
   const int storage = storage_of_flags(flags);
   if (storage != spec) {
+    ctx->quant_bits = 0;
     if ((rc = alloc_matrix(ctx, n, storage))) return rc;
     CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
                            ctx->stream));
@@ -509,7 +572,7 @@ constexpr int kNarrowFallback = 1000;  // upload_narrow: a value needs a wider t
 // copy exactly as from fp64 (the narrowing is exact).  Any value that does
 // not fit returns kNarrowFallback and the caller redoes the fp64 upload.
 template <class T>
-int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, int32_t ndtype) {
+int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, int32_t ndtype, float probe_amax) {
   const size_t row_bytes = static_cast<size_t>(n) * sizeof(T);
   const size_t total = row_bytes * static_cast<size_t>(n);
   if (ctx->stage.bytes < total) {
@@ -549,6 +612,11 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     const int rc = alloc_matrix(ctx, n, storage);
     if (rc) return rc;
   }
+  QuantTarget qt;
+  {
+    const int rc = prepare_quant(ctx, storage, probe_amax, &qt);
+    if (rc) return rc;
+  }
   LayoutSource src;
   src.kind = 0;
   src.src = ctx->stage.p;
@@ -578,7 +646,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     CK(cudaEventRecord(ctx->ev_chunk[b], ctx->copy_stream));
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_chunk[b], 0));
     CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
-                           ctx->d.ld, ctx->chunk_flags + k, ctx->stream, ctx->flags_dev + 2));
+                           ctx->d.ld, ctx->chunk_flags + k, ctx->stream, ctx->flags_dev + 2, qt));
     ++ctx->launches;
   }
   std::vector<uint32_t> fl(nchunks);
@@ -588,6 +656,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   for (uint32_t f : fl) all |= f;
   const int final_storage = storage_of_flags(all);
   if (final_storage != storage) {  // (cannot widen: every value passed T's rule; narrower is possible)
+    ctx->quant_bits = 0;
     int rc = alloc_matrix(ctx, n, final_storage);
     if (rc) return rc;
     CK(launch_build_layout(src, n, 0, n, final_storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
@@ -615,19 +684,30 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
     if (!ctx->pool) ctx->pool = new HostPool(upload_threads());
     const int T_ = ctx->pool->size();
     std::vector<uint32_t> pf(static_cast<size_t>(T_), 0u);
+    std::vector<double> pm(static_cast<size_t>(T_), 0.0);
     ctx->pool->run([&](int t) {
       uint32_t f = 0;
-      for (size_t i = probe * t / T_; i < probe * (t + 1) / T_; ++i) f |= host_entry_flags(a[i]);
+      double m = 0.0;
+      for (size_t i = probe * t / T_; i < probe * (t + 1) / T_; ++i) {
+        f |= host_entry_flags(a[i]);
+        if (std::isfinite(a[i])) m = std::max(m, std::fabs(a[i]));
+      }
       pf[t] = f;
+      pm[t] = m;
     });
     uint32_t f = 0;
+    double pmax = 0.0;
     for (uint32_t x : pf) f |= x;
+    for (double x : pm) pmax = std::max(pmax, x);
+    // max |a| of the probe rows as a float rounded up (like the device's __double2float_ru)
+    float pamax = static_cast<float>(pmax);
+    if (static_cast<double>(pamax) < pmax) pamax = std::nextafter(pamax, INFINITY);
     if (f & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
     const int spec = storage_of_flags(f);
     rc = kNarrowFallback;
-    if (spec == kI16) rc = upload_narrow<int16_t>(ctx, a, n, kI16, LSAPGPU_I16);
-    else if (spec == kI32) rc = upload_narrow<int32_t>(ctx, a, n, kI32, LSAPGPU_I32);
-    else if (spec == kF32) rc = upload_narrow<float>(ctx, a, n, kF32, LSAPGPU_F32);
+    if (spec == kI16) rc = upload_narrow<int16_t>(ctx, a, n, kI16, LSAPGPU_I16, pamax);
+    else if (spec == kI32) rc = upload_narrow<int32_t>(ctx, a, n, kI32, LSAPGPU_I32, pamax);
+    else if (spec == kF32) rc = upload_narrow<float>(ctx, a, n, kF32, LSAPGPU_F32, pamax);
     if (rc != kNarrowFallback) return rc;
   }
   const size_t es = src_size(dtype);
@@ -674,6 +754,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
   if (!pinned && !ctx->pool) ctx->pool = new HostPool(upload_threads());
 
   int storage = -1;
+  QuantTarget qt;
   LayoutSource src;
   src.kind = 0;
   src.src = ctx->stage.p;
@@ -701,24 +782,27 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
     CK(cudaEventRecord(done, ctx->copy_stream));
     CK(cudaStreamWaitEvent(ctx->stream, done, 0));
     if (k == 0) {  // speculate the storage from the first rows
-      CK(launch_classify(src, n, r0, std::min<int64_t>(rows, 64), ctx->chunk_flags + k, ctx->stream));
+      CK(cudaMemsetAsync(ctx->flags_dev + 3, 0, sizeof(uint32_t), ctx->stream));
+      CK(launch_classify(src, n, r0, std::min<int64_t>(rows, 64), ctx->chunk_flags + k, ctx->stream,
+                         ctx->flags_dev + 3));
       ++ctx->launches;
-      uint32_t f0 = 0;
+      uint32_t f0 = 0, pa = 0;
       CK(cpy(ctx, &f0, ctx->chunk_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cpy(ctx, &pa, ctx->flags_dev + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       if (f0 & 1u) {
         CK(cudaStreamSynchronize(ctx->copy_stream));
         return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
       }
       storage = storage_of_flags(f0);
-      if ((rc = alloc_matrix(ctx, n, storage))) {
+      if ((rc = alloc_matrix(ctx, n, storage)) || (rc = prepare_quant(ctx, storage, bits_to_float(pa), &qt))) {
         cudaStreamSynchronize(ctx->copy_stream);
         return rc;
       }
     }
     CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
                            const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->chunk_flags + k, ctx->stream,
-                           ctx->flags_dev + 2));
+                           ctx->flags_dev + 2, qt));
     ++ctx->launches;
   }
   std::vector<uint32_t> fl(nchunks);
@@ -729,6 +813,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
   if (all & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
   const int final_storage = storage_of_flags(all);
   if (final_storage != storage) {  // a later chunk needs a wider type: rebuild everything
+    ctx->quant_bits = 0;
     if ((rc = alloc_matrix(ctx, n, final_storage))) return rc;
     CK(launch_build_layout(src, n, 0, n, final_storage, const_cast<void*>(ctx->d.A),
                            const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->stream));

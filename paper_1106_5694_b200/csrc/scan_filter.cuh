@@ -195,7 +195,17 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
                  reinterpret_cast<const unsigned char*>(Qg + static_cast<int64_t>(cur.agent) * ld) + off, sz,
                  &row_full[rb]);
       }
-      if (q + 1 < stages) nxt = item_of(q + 1);
+      if (q + 1 < stages) {
+        nxt = item_of(q + 1);
+        // one row buffer: pull the next row into L2 now, so its (exposed)
+        // staging copy after this item streams from L2 rather than HBM
+        if (RB == 1)
+          for (int pc = lane; pc < pieces; pc += 32) {
+            const uint32_t off = static_cast<uint32_t>(pc) * kPiece;
+            l2_prefetch(reinterpret_cast<const unsigned char*>(Qg + static_cast<int64_t>(nxt.agent) * ld) + off,
+                        (rbytes - off) < kPiece ? (rbytes - off) : kPiece);
+          }
+      }
     }
   } else if (warp == kFW + 1) {
     // ---------------- chunk producer: QT chunk c of item q into the slot ring ----------------
@@ -245,15 +255,34 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       ta.init();
       tj.init();
       if (cnt <= qcap) {
-        for (int e = lane; e < cnt; e += 32) {
-          const unsigned long long ent = queue[par * qcap + e];
-          const int32_t p = static_cast<int32_t>(ent & 0xFFFFFFFFull);
-          const int32_t t = static_cast<int32_t>(ent >> 32);
-          const double gv = static_cast<double>(arow[t]);
-          const double xv = static_cast<double>(xrow[p]);
-          const double cv = static_cast<double>(acur_g[p]);
-          ta.add(delta4(gv, s, xv, cv), t);
-          tj.add(delta4(xv, s, gv, cv), p);
+        // four entries per lane per round, every global load of a round in
+        // flight together (the entries are random positions: one HBM round
+        // trip per round instead of one per entry)
+        for (int e0 = 0; e0 < cnt; e0 += 128) {
+          int32_t pp[4], tt[4];
+          E gg[4], xx[4], cc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * 32 + lane;
+            const unsigned long long ent = e < cnt ? queue[par * qcap + e] : 0ull;
+            pp[u] = static_cast<int32_t>(ent & 0xFFFFFFFFull);
+            tt[u] = e < cnt ? static_cast<int32_t>(ent >> 32) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = tt[u] >= 0;
+            gg[u] = ok ? arow[tt[u]] : E(0);
+            xx[u] = ok ? xrow[pp[u]] : E(0);
+            cc[u] = ok ? acur_g[pp[u]] : E(0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (tt[u] < 0) continue;
+            const double gv = static_cast<double>(gg[u]), xv = static_cast<double>(xx[u]),
+                         cv = static_cast<double>(cc[u]);
+            ta.add(delta4(gv, s, xv, cv), tt[u]);
+            tj.add(delta4(xv, s, gv, cv), pp[u]);
+          }
         }
       } else {  // queue overflow (heavy ties): exact scan of the whole item
         ++overflows;
@@ -386,8 +415,12 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
         x1 = x0;
       }
     };
-    uint4 n0, n1;
+    // two chunks of aux in flight: L2 latency under this load exceeds one
+    // chunk's compute (long-scoreboard stalls with a one-chunk lead)
+    uint4 n0, n1, f0, f1;
+    int32_t cnext = nch > 1 ? 1 : 0;  // chunk held in (f0, f1)
     load_aux(0, n0, n1);
+    load_aux(cnext, f0, f1);
     for (int32_t q = 0; q < stages; ++q) {
       const int rb = q % RB;
       const int par = q & 1;
@@ -399,7 +432,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       int32_t tshare = kFNeg;  // last read of tmax[par]
       for (int32_t c = 0; c < nch; ++c) {
         const uint4 a0 = n0, a1 = n1;
-        load_aux(c + 1 < nch ? c + 1 : 0, n0, n1);  // next chunk (or chunk 0 of the next item)
+        n0 = f0;
+        n1 = f1;
+        cnext = cnext + 1 < nch ? cnext + 1 : 0;  // chunk c + 2 (wrapping into the next item)
+        load_aux(cnext, f0, f1);
         mbar_wait_backoff(&slot_full[s], fph, 20);
         const unsigned char* sb = slots + s * kSlotBytes;
         uint4 qv;

@@ -104,16 +104,25 @@ struct LayoutSource {
 };
 // flags bit0: non-finite present, bit1: not int16-exact, bit2: not int32 (<2^29) exact,
 // bit3: not fp32-exact.
+// amax (nullable): atomicMax of the float bits of every |entry| rounded up
 cudaError_t launch_classify(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
-                            uint32_t* flags, cudaStream_t st);
+                            uint32_t* flags, cudaStream_t st, uint32_t* amax = nullptr);
+// Quantized filter copies the layout pass writes alongside A / AT (bits 0: none)
+struct QuantTarget {
+  void* Q = nullptr;
+  void* QT = nullptr;
+  double scale = 0.0;
+  int bits = 0;
+};
 cudaError_t launch_build_layout(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows,
                                 int storage, void* A, void* AT, int64_t ld, cudaStream_t st);
 cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaStream_t st);
 // classify + build in one pass for a speculated storage type (flags as launch_classify)
-// amax (nullable): atomicMax of the float bits of every |entry| rounded up (the filter's scale)
+// amax (nullable): atomicMax of the float bits of every |entry| rounded up (the filter's scale);
+// qt.bits != 0: also write the quantized copies Q / QT
 cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
                                 void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st,
-                                uint32_t* amax = nullptr);
+                                uint32_t* amax = nullptr, QuantTarget qt = QuantTarget{});
 // Q = ceil(A * scale), QT = ceil(AT * scale) as int16 (qbits 16) or int8 (qbits 8), padding zeroed
 cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st);
 cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st);  // tau, acur from sigma

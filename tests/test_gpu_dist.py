@@ -229,3 +229,41 @@ def test_bench_two_ranks_sharded_block(tmp_path, exchange):
     assert blk["sigma_sha_matches_golden"] is True
     assert blk["full_sweep_ms"] > 0 and blk["scan_kernel"] == "filter"
     assert ("peer-memory" in blk["transport"]) == (exchange == "p2p")
+
+
+def test_sharded_large_filter_equals_single_gpu(tmp_path):
+    """The sharded solve at a C5-like size on the filter scan (n = 60000
+    fp32, int8 copies, each rank scanning its share of the items): both
+    ranks return the single-GPU sigma bit for bit (peer transport, ranks as
+    threads on GPU 0 -- two 36 GB replicas)."""
+    import hashlib
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, json, hashlib, threading; sys.path.insert(0, %r)\n"
+        "import paper_1106_5694_b200 as g\n"
+        "from paper_1106_5694_b200.dist import ThreadPeerExchange\n"
+        "n = 60000\n"
+        "h = lambda s: hashlib.sha256(s.tobytes()).hexdigest()\n"
+        "ctx = g.Context(0); ctx.generate('f32', n, 0)\n"
+        "ref = ctx.solve(g.ParallelConfig(seed=0)); plan = ctx.scan_plan(); ctx.close()\n"
+        "ex = ThreadPeerExchange.group(2); out = [None, None]\n"
+        "def run(r):\n"
+        "    c = g.Context(0); c.generate('f32', n, 0)\n"
+        "    out[r] = c.solve(g.ParallelConfig(seed=0), dist=ex[r]); c.close()\n"
+        "th = [threading.Thread(target=run, args=(r,)) for r in range(2)]\n"
+        "[t.start() for t in th]; [t.join() for t in th]\n"
+        "[e.free() for e in ex]\n"
+        "print(json.dumps({'plan': plan, 'ref': h(ref.assignment.sigma), 'value': ref.assignment.value,\n"
+        "                  'ranks': [h(o.assignment.sigma) for o in out], 'values': [o.assignment.value for o in out]}))\n"
+        % root)
+    env = dict(os.environ, LSAPGPU_FILTER_BITS="8")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    out = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out["plan"]["kernel"] == "filter" and out["plan"]["filter"] == 8
+    assert out["ranks"] == [out["ref"], out["ref"]]
+    assert out["values"] == [out["value"], out["value"]]

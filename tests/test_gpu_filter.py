@@ -36,10 +36,16 @@ mats = [
     ("tiny", f32(rng.uniform(0.0, 1.0, (900, 900)) * 1e-36)),
     ("ties", f32(rng.integers(0, 4, (1500, 1500)) * 0.375 + 0.1)),
     ("spiky", f32(np.where(rng.random((1200, 1200)) < 0.01, 1e6, rng.random((1200, 1200))))),
+    # the first 64 rows (the probe that picks the layout pass's quantization
+    # scale) smaller than the rest: the fused copies are redone separately
+    ("probe-small", f32(rng.random((1500, 1500)) * np.where(np.arange(1500) < 64, 1e-3, 1.0)[:, None])),
+    ("probe-large", f32(rng.random((1500, 1500)) * np.where(np.arange(1500) < 64, 1.0, 1e-3)[:, None])),
 ]
-for name, a in mats:
+import torch
+for k, (name, a) in enumerate(mats):
     n = a.shape[0]
-    ctx.set_matrix(a)
+    # alternate the three layout paths: host (narrowed on the host), device fp64 source
+    ctx.set_matrix(a if (k & 1) == 0 else torch.from_numpy(a).cuda())
     assert ctx.scan_plan()["filter"] in (8, 16), (name, ctx.scan_plan())
     for eps in (0.0, 1e-3):
         s = o.random_perm(n, 4)
