@@ -44,6 +44,7 @@ __attribute__((target("avx2"))) bool narrow_int_avx2(const double* __restrict__ 
   const __m256d hi = _mm256_set1_pd(lim), lo = _mm256_set1_pd(-lim);
   __m256d ok = _mm256_castsi256_pd(_mm256_set1_epi64x(-1));
   size_t i = 0;
+  const bool nt = (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (8 * sizeof(T)) % 16 == 0;
   for (; i + 8 <= cnt; i += 8) {
     const __m256d v0 = _mm256_loadu_pd(src + i), v1 = _mm256_loadu_pd(src + i + 4);
     const __m256d in0 = _mm256_and_pd(_mm256_cmp_pd(v0, lo, _CMP_GE_OQ), _mm256_cmp_pd(v0, hi, _CMP_LE_OQ));
@@ -53,13 +54,23 @@ __attribute__((target("avx2"))) bool narrow_int_avx2(const double* __restrict__ 
     const __m256d e0 = _mm256_cmp_pd(_mm256_cvtepi32_pd(x0), v0, _CMP_EQ_OQ);
     const __m256d e1 = _mm256_cmp_pd(_mm256_cvtepi32_pd(x1), v1, _CMP_EQ_OQ);
     ok = _mm256_and_pd(ok, _mm256_and_pd(_mm256_and_pd(in0, e0), _mm256_and_pd(in1, e1)));
+    // streaming (non-temporal) stores when the destination is 16-byte
+    // aligned: the pinned ring is written once and read by the DMA engine,
+    // so reading its lines into the cache first (write-allocate) is waste
     if constexpr (sizeof(T) == 2) {
-      _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), _mm_packs_epi32(x0, x1));
+      if (nt) _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_packs_epi32(x0, x1));
+      else _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), _mm_packs_epi32(x0, x1));
     } else {
-      _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), x0);
-      _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i + 4), x1);
+      if (nt) {
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), x0);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4), x1);
+      } else {
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), x0);
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i + 4), x1);
+      }
     }
   }
+  if (nt) _mm_sfence();
   const bool vok = _mm256_movemask_pd(ok) == 0xF;
   return narrow_scalar<T>(src + i, dst + i, cnt - i, lim) && vok;
 }
@@ -70,6 +81,7 @@ __attribute__((target("avx2"))) bool narrow_f32_avx2(const double* __restrict__ 
   const __m256d absmask = _mm256_castsi256_pd(_mm256_set1_epi64x(0x7fffffffffffffffLL));
   __m256d ok = _mm256_castsi256_pd(_mm256_set1_epi64x(-1));
   size_t i = 0;
+  const bool nt = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
   for (; i + 8 <= cnt; i += 8) {
     const __m256d v0 = _mm256_loadu_pd(src + i), v1 = _mm256_loadu_pd(src + i + 4);
     const __m256d in0 = _mm256_cmp_pd(_mm256_and_pd(v0, absmask), mx, _CMP_LE_OQ);
@@ -79,9 +91,15 @@ __attribute__((target("avx2"))) bool narrow_f32_avx2(const double* __restrict__ 
     const __m256d e0 = _mm256_cmp_pd(_mm256_cvtps_pd(f0), v0, _CMP_EQ_OQ);
     const __m256d e1 = _mm256_cmp_pd(_mm256_cvtps_pd(f1), v1, _CMP_EQ_OQ);
     ok = _mm256_and_pd(ok, _mm256_and_pd(_mm256_and_pd(in0, e0), _mm256_and_pd(in1, e1)));
-    _mm_storeu_ps(dst + i, f0);
-    _mm_storeu_ps(dst + i + 4, f1);
+    if (nt) {
+      _mm_stream_ps(dst + i, f0);
+      _mm_stream_ps(dst + i + 4, f1);
+    } else {
+      _mm_storeu_ps(dst + i, f0);
+      _mm_storeu_ps(dst + i + 4, f1);
+    }
   }
+  if (nt) _mm_sfence();
   const bool vok = _mm256_movemask_pd(ok) == 0xF;
   return narrow_scalar<float>(src + i, dst + i, cnt - i, 0.0) && vok;
 }

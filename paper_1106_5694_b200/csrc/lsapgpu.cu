@@ -631,8 +631,8 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     if (k >= kRing) CK(cudaEventSynchronize(ctx->ev_chunk[b]));  // ring slot's previous DMA done
     T* pin = static_cast<T*>(ctx->ring[b]);
     const double* hsrc = data + static_cast<size_t>(r0) * static_cast<size_t>(n);
-    ctx->pool->run([&](int t) {
-      const size_t a = cnt * t / T_, e = cnt * (t + 1) / T_;
+    ctx->pool->run([&](int t) {  // slices of whole 16-byte groups: streaming stores need the alignment
+      const size_t a = cnt * t / T_ / 8 * 8, e = t + 1 == T_ ? cnt : cnt * (t + 1) / T_ / 8 * 8;
       okv[t] = narrow_block(hsrc + a, pin + a, e - a) ? 1 : 0;
     });
     for (int t = 0; t < T_; ++t)
@@ -1047,6 +1047,7 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
   ctx->d.pdl = 1;  // programmatic dependent launch for the inner-loop kernels (LSAPGPU_PDL=0: off)
   if (const char* e = std::getenv("LSAPGPU_PDL")) ctx->d.pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSAPGPU_FILTER_CHECK")) ctx->d.filter_check = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("LSAPGPU_FILTER_FLAGS")) ctx->d.filter_flags = std::atoi(e);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||

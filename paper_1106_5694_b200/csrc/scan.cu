@@ -21,9 +21,9 @@ cudaError_t launch_scan_filter_typed(const DevState& d, const ScanPlan& p, int f
 // quantized A rows, a ring of QT chunk slots, two candidate queues.
 constexpr int32_t kFilterChunk = 4096;
 constexpr int kFilterQueueMax = 1024;
-size_t filter_smem(int64_t ld, int qbytes, int rb, int ns, int qcap) {
+size_t filter_smem(int64_t ld, int qbytes, int rb, int ns, int qcap, int32_t chunk = kFilterChunk) {
   const size_t row = (static_cast<size_t>(ld) * qbytes + 127) / 128 * 128;
-  const size_t slot = static_cast<size_t>(kFilterChunk) * qbytes;
+  const size_t slot = static_cast<size_t>(chunk) * qbytes;
   return rb * row + ns * slot + 2 * static_cast<size_t>(qcap) * 8 + (rb + 2 * 8 + 4) * 8;
 }
 
@@ -169,26 +169,38 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     if (const char* r = std::getenv("LSAPGPU_FILTER_RB")) want_rb = std::atoi(r);
     int want_q = -1;
     if (const char* qq = std::getenv("LSAPGPU_FILTER_QUEUE")) want_q = std::max(0, std::min(kFilterQueueMax, std::atoi(qq)));
-    // prefer int16 copies, double-buffered rows, >= 4 slots, a 1024-entry
-    // queue; shrink the queue (to 512) before giving up a row buffer
+    // consumer geometry: 16 warps x 8 positions per lane (608 threads), or
+    // LSAPGPU_FILTER_WARPS=24: 24 warps x 4 (864 threads), the per-SM work
+    // in more, shorter warps
+    int threads = 32 * 19;
+    int32_t chunk = kFilterChunk;
+    if (const char* w = std::getenv("LSAPGPU_FILTER_WARPS"))
+      if (std::atoi(w) == 24) {
+        threads = 32 * 27;
+        chunk = 24 * 32 * 4;
+      }
+    // prefer int16 copies, then double-buffered rows with a 1024-entry queue
+    // and >= 3 slots, then one row buffer (its refill streams from L2: the
+    // next row is prefetched; measured faster at C5 than two rows with a
+    // 3-slot ring), then a 512-entry queue
     bool done = false;
     for (int qb : {2, 1}) {
       if (want_bits && want_bits != 8 * qb) continue;
-      for (int rb : {2, 1}) {
-        if (want_rb && want_rb != rb) continue;
-        for (int qcap : {kFilterQueueMax, kFilterQueueMax / 2}) {
-          if (want_q >= 0) qcap = want_q;
+      for (int qcap : {kFilterQueueMax, kFilterQueueMax / 2}) {
+        if (want_q >= 0) qcap = want_q;
+        for (int rb : {2, 1}) {
+          if (want_rb && want_rb != rb) continue;
           int ns = 8;
-          while (ns >= 3 && filter_smem(d.ld, qb, rb, ns, qcap) > limit) --ns;
+          while (ns >= 3 && filter_smem(d.ld, qb, rb, ns, qcap, chunk) > limit) --ns;
           if (ns < 3) continue;
           p.filter = 8 * qb;
           p.m = rb;
           p.bufs = ns;
           p.resident = 0;
           p.passes = 1;
-          p.chunk = kFilterChunk;
-          p.threads = 32 * 19;
-          p.smem = filter_smem(d.ld, qb, rb, ns, qcap);
+          p.chunk = chunk;
+          p.threads = threads;
+          p.smem = filter_smem(d.ld, qb, rb, ns, qcap, chunk);
           p.ctas = num_sms;
           p.max_segments = 1;
           p.l2_prefetch = 0;

@@ -93,8 +93,45 @@ __device__ __forceinline__ int32_t eps_gate(double sv, double eps, double S) {
 
 // smem: rows [RB][ld] Q | slots [NS] x QT chunk [C] Q | queue [2][qcap] u64 |
 //       row_full[RB], slot_full[NS], slot_empty[NS], item_done[2], queue_free[2] mbarriers
-template <class E, class Q, int RB>
-__global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState st, int full, int NS, int qcap) {
+// W consumer warps of V positions per lane: a chunk is W * 32 * V positions.
+template <int V>
+struct AuxW {
+  uint32_t w[V];
+};
+template <int V>
+__device__ __forceinline__ void ld_aux(AuxW<V>& a, const uint32_t* p, bool ok) {
+#pragma unroll
+  for (int k = 0; k < V / 4; ++k) {
+    const uint4 x = ok ? __ldcg(reinterpret_cast<const uint4*>(p) + k) : make_uint4(0u, 0u, 0u, 0u);
+    a.w[4 * k] = x.x;
+    a.w[4 * k + 1] = x.y;
+    a.w[4 * k + 2] = x.z;
+    a.w[4 * k + 3] = x.w;
+  }
+}
+// V consecutive Q elements of a staged QT chunk, as the first V*sizeof(Q) bytes of a uint4
+template <class Q, int V>
+__device__ __forceinline__ uint4 lds_q(const unsigned char* p) {
+  constexpr int kBytes = V * static_cast<int>(sizeof(Q));
+  if constexpr (kBytes == 16) {
+    return *reinterpret_cast<const uint4*>(p);
+  } else if constexpr (kBytes == 8) {
+    const uint2 h = *reinterpret_cast<const uint2*>(p);
+    return make_uint4(h.x, h.y, 0u, 0u);
+  } else {
+    return make_uint4(*reinterpret_cast<const uint32_t*>(p), 0u, 0u, 0u);
+  }
+}
+
+template <class E, class Q, int RB, int W, int V>
+__global__ void __launch_bounds__(32 * (W + 3), 1)
+    pair_scan_filter_kernel(DevState st, int full, int NS, int qcap) {
+  // the geometry of this instantiation (shadowing the default constants)
+  constexpr int kFW = W;
+  constexpr int kFV = V;
+  constexpr int kFBlk = 32 * V;
+  constexpr int32_t kFChunk = W * 32 * V;
+  constexpr int kFThreads = 32 * (W + 3);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int32_t n = st.n;
   const int64_t ld = st.ld;
@@ -147,7 +184,9 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       mbar_init(&slot_empty[k], kFW);
     }
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&item_done[k], kFW * 32);  // every consumer lane arrives (its own queue stores released)
+      // every consumer lane arrives (its own queue stores released), or with
+      // LSAPGPU_FILTER_FLAGS bit 0 one lane per warp after a CTA fence on every lane
+      mbar_init(&item_done[k], (st.filter_flags & 1) ? kFW : kFW * 32);
       mbar_init(&queue_free[k], 1);
       qn[k] = 0;
       tmax[k] = kFNeg;
@@ -405,22 +444,16 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
     const int32_t lo = warp * kFBlk + lane * kFV;  // position offset within a chunk
     int s = 0;
     uint32_t fph = 0;  // slot_full phase parity
-    auto load_aux = [&](int32_t c, uint4& x0, uint4& x1) {
+    auto load_aux = [&](int32_t c, AuxW<kFV>& x) {
       const int64_t p = static_cast<int64_t>(c) * kFChunk + lo;
-      if (p < n) {
-        x0 = __ldcg(reinterpret_cast<const uint4*>(aux_g + p));
-        x1 = __ldcg(reinterpret_cast<const uint4*>(aux_g + p + 4));
-      } else {
-        x0 = make_uint4(0u, 0u, 0u, 0u);
-        x1 = x0;
-      }
+      ld_aux<kFV>(x, aux_g + p, p < n);
     };
     // two chunks of aux in flight: L2 latency under this load exceeds one
     // chunk's compute (long-scoreboard stalls with a one-chunk lead)
-    uint4 n0, n1, f0, f1;
-    int32_t cnext = nch > 1 ? 1 : 0;  // chunk held in (f0, f1)
-    load_aux(0, n0, n1);
-    load_aux(cnext, f0, f1);
+    AuxW<kFV> nx, fx;
+    int32_t cnext = nch > 1 ? 1 : 0;  // chunk held in fx
+    load_aux(0, nx);
+    load_aux(cnext, fx);
     for (int32_t q = 0; q < stages; ++q) {
       const int rb = q % RB;
       const int par = q & 1;
@@ -431,21 +464,14 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       int32_t T = t0;
       int32_t tshare = kFNeg;  // last read of tmax[par]
       for (int32_t c = 0; c < nch; ++c) {
-        const uint4 a0 = n0, a1 = n1;
-        n0 = f0;
-        n1 = f1;
+        const AuxW<kFV> ax = nx;
+        nx = fx;
         cnext = cnext + 1 < nch ? cnext + 1 : 0;  // chunk c + 2 (wrapping into the next item)
-        load_aux(cnext, f0, f1);
+        load_aux(cnext, fx);
         mbar_wait_backoff(&slot_full[s], fph, 20);
         const unsigned char* sb = slots + s * kSlotBytes;
-        uint4 qv;
-        if constexpr (sizeof(Q) == 2) {
-          qv = *reinterpret_cast<const uint4*>(sb + lo * 2);
-        } else {
-          const uint2 h = *reinterpret_cast<const uint2*>(sb + lo);
-          qv = make_uint4(h.x, h.y, 0u, 0u);
-        }
-        const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const uint4 qv = lds_q<Q, kFV>(sb + lo * static_cast<int>(sizeof(Q)));
+        const uint32_t(&aw)[kFV] = ax.w;
         const int32_t p0 = c * kFChunk + lo;
         // aux low 17 bits = the BYTE offset of Q[i][t] in the staged row, so a
         // gather is one LOP3 + one LDS [reg + uniform base]
@@ -504,7 +530,13 @@ __global__ void __launch_bounds__(kFThreads, 1) pair_scan_filter_kernel(DevState
       }
       // every lane arrives after its last use of row buffer rb and its own
       // queue stores: releases the row and hands the queue to the verifier
-      mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
+      if (st.filter_flags & 1) {
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
+      } else {
+        mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
+      }
     }
   }
   __syncthreads();
@@ -536,14 +568,22 @@ __global__ void filter_aux_kernel(DevState st) {
   }
 }
 
-template <class E, class Q, int RB>
+template <class E, class Q, int RB, int W, int V>
 cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
   cudaError_t e = launch_pdl(filter_aux_kernel<E, Q>, dim3(p.ctas), dim3(256), 0, st, d.pdl, d);
   if (e != cudaSuccess) return e;
-  auto k = pair_scan_filter_kernel<E, Q, RB>;
+  auto k = pair_scan_filter_kernel<E, Q, RB, W, V>;
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;
-  return launch_pdl(k, dim3(p.ctas), dim3(kFThreads), p.smem, st, d.pdl, d, full, p.bufs, p.filter_queue);
+  return launch_pdl(k, dim3(p.ctas), dim3(32 * (W + 3)), p.smem, st, d.pdl, d, full, p.bufs, p.filter_queue);
+}
+
+// consumer geometry from the plan's thread count: 608 = 16 warps x 8
+// positions per lane, 992 = 28 warps x 4 (more warps to hide latency)
+template <class E, class Q, int RB>
+cudaError_t launch_filter_g(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  return p.threads == 32 * 27 ? launch_filter_t<E, Q, RB, 24, 4>(d, p, full, st)
+                              : launch_filter_t<E, Q, RB, 16, 8>(d, p, full, st);
 }
 
 }  // namespace scan_detail
@@ -551,10 +591,10 @@ cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cuda
 template <class E>
 cudaError_t launch_scan_filter_typed(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
   if (p.filter == 16)
-    return p.m == 2 ? scan_detail::launch_filter_t<E, int16_t, 2>(d, p, full, st)
-                    : scan_detail::launch_filter_t<E, int16_t, 1>(d, p, full, st);
-  return p.m == 2 ? scan_detail::launch_filter_t<E, int8_t, 2>(d, p, full, st)
-                  : scan_detail::launch_filter_t<E, int8_t, 1>(d, p, full, st);
+    return p.m == 2 ? scan_detail::launch_filter_g<E, int16_t, 2>(d, p, full, st)
+                    : scan_detail::launch_filter_g<E, int16_t, 1>(d, p, full, st);
+  return p.m == 2 ? scan_detail::launch_filter_g<E, int8_t, 2>(d, p, full, st)
+                  : scan_detail::launch_filter_g<E, int8_t, 1>(d, p, full, st);
 }
 
 }  // namespace lsapgpu
