@@ -9,6 +9,7 @@ import sys, json; sys.path.insert(0, %r)
 import paper_1106_5694_b200 as g
 n = %d
 ctx = g.Context(0); ctx.generate("f32", n, 0)
+ctx.solve(g.ParallelConfig(seed=0))  # warm: first touch of every buffer, graph build
 ctx.set_scan_timing(True)
 r = ctx.solve(g.ParallelConfig(seed=0, use_graph=False))
 ctx.set_scan_timing(False)
