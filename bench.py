@@ -484,6 +484,11 @@ def run_ours(args, wl) -> None:
         "traffic_source": tr.get("source") if tr else None,
         "plan": plan,
     }
+    if plan["filter"]:  # the filter kernel streams quantized copies: its actual rate beside the algorithmic one
+        qbytes = full_bytes * (plan["filter"] // 8) / eb
+        roofline["full_sweep"]["streamed_bytes_per_launch"] = qbytes
+        roofline["full_sweep"]["streamed_gbs"] = (qbytes * tm["full_launches"]) / (tm["full_ms"] * 1e-3) / 1e9 \
+            if tm["full_ms"] > 0 else None
 
     # extension (not the headline): the same step from the device greedy
     # initial assignment instead of the reference's initial_random; its result

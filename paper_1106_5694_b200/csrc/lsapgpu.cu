@@ -421,14 +421,13 @@ float bits_to_float(uint32_t b) {
   return f;
 }
 
-// Before a layout pass of fp32 storage: if the scan plan for this matrix uses
+// Before a layout pass: if the scan plan for this matrix uses
 // the filter copies, size them and pick the scale from the probe rows' max
 // |a| so the layout pass writes Q / QT itself (no separate quantize pass);
 // finish_matrix checks the scale against the whole matrix's max afterwards.
 int prepare_quant(lsapgpu_ctx* ctx, int storage, float probe_amax, QuantTarget* qt) {
   *qt = QuantTarget{};
   ctx->quant_bits = 0;
-  if (storage != kF32) return LSAPGPU_OK;
   DevState tmp = ctx->d;
   tmp.storage = storage;
   const ScanPlan p = plan_scan(tmp, ctx->num_sms);
@@ -1047,7 +1046,6 @@ int lsapgpu_create(lsapgpu_ctx** out, int device) {
   ctx->d.pdl = 1;  // programmatic dependent launch for the inner-loop kernels (LSAPGPU_PDL=0: off)
   if (const char* e = std::getenv("LSAPGPU_PDL")) ctx->d.pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSAPGPU_FILTER_CHECK")) ctx->d.filter_check = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("LSAPGPU_FILTER_FLAGS")) ctx->d.filter_flags = std::atoi(e);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->ctrl_dev, sizeof(Ctrl)) != cudaSuccess ||
       cudaMallocHost(&ctx->ctrl_host, sizeof(Ctrl)) != cudaSuccess ||

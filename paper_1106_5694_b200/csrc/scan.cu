@@ -154,14 +154,14 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       if (p.l2_prefetch >= 32 / m) p.l2_prefetch = 32 / m - 1;
     }
   }
-  // Long rows of float storage: the quantized-filter kernel (scan_filter.cuh)
-  // reads int16 (or int8) copies of the rows and verifies the few surviving
-  // candidates exactly.  LSAPGPU_SCAN_FILTER=0 disables it, =2 forces it at
+  // Long rows (any storage the resident kernel cannot hold on chip): the
+  // quantized-filter kernel (scan_filter.cuh) reads int16 (or int8) copies
+  // of the rows and verifies the few surviving candidates exactly.  LSAPGPU_SCAN_FILTER=0 disables it, =2 forces it at
   // any n (tests); LSAPGPU_FILTER_BITS=8|16, LSAPGPU_FILTER_RB=1|2 and
   // LSAPGPU_FILTER_QUEUE=k pin the geometry so tests reach every path.
   int filt = 1;
   if (const char* f = std::getenv("LSAPGPU_SCAN_FILTER")) filt = std::atoi(f);
-  if (filt && d.storage == kF32 && d.n < 131072 && (!p.resident || filt >= 2) &&
+  if (filt && d.n < 131072 && (!p.resident || filt >= 2) &&
       !std::getenv("LSAPGPU_SCAN_BUDGET")) {
     const size_t limit = 232448 - 8 * 1024;  // dynamic smem next to the kernel's static ~7 KB
     int want_bits = 0, want_rb = 0;
@@ -169,16 +169,8 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     if (const char* r = std::getenv("LSAPGPU_FILTER_RB")) want_rb = std::atoi(r);
     int want_q = -1;
     if (const char* qq = std::getenv("LSAPGPU_FILTER_QUEUE")) want_q = std::max(0, std::min(kFilterQueueMax, std::atoi(qq)));
-    // consumer geometry: 16 warps x 8 positions per lane (608 threads), or
-    // LSAPGPU_FILTER_WARPS=24: 24 warps x 4 (864 threads), the per-SM work
-    // in more, shorter warps
-    int threads = 32 * 19;
-    int32_t chunk = kFilterChunk;
-    if (const char* w = std::getenv("LSAPGPU_FILTER_WARPS"))
-      if (std::atoi(w) == 24) {
-        threads = 32 * 27;
-        chunk = 24 * 32 * 4;
-      }
+    const int threads = 32 * 19;  // 16 consumer warps x 8 positions per lane + 3 role warps
+    const int32_t chunk = kFilterChunk;
     // prefer int16 copies, then double-buffered rows with a 1024-entry queue
     // and >= 3 slots, then one row buffer (its refill streams from L2: the
     // next row is prefetched; measured faster at C5 than two rows with a
@@ -218,8 +210,14 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
 
 cudaError_t launch_scan(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
   if (p.filter) {
-    if (d.storage != kF32 || !d.Q || !d.QT || !d.aux) return cudaErrorInvalidValue;
-    return launch_scan_filter_typed<float>(d, p, full, st);
+    if (!d.Q || !d.QT || !d.aux) return cudaErrorInvalidValue;
+    switch (d.storage) {
+      case kI16: return launch_scan_filter_typed<int16_t>(d, p, full, st);
+      case kI32: return launch_scan_filter_typed<int32_t>(d, p, full, st);
+      case kF32: return launch_scan_filter_typed<float>(d, p, full, st);
+      case kF64: return launch_scan_filter_typed<double>(d, p, full, st);
+      default: return cudaErrorInvalidValue;
+    }
   }
   if (p.resident) {
     switch (d.storage) {

@@ -184,9 +184,7 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
       mbar_init(&slot_empty[k], kFW);
     }
     for (int k = 0; k < 2; ++k) {
-      // every consumer lane arrives (its own queue stores released), or with
-      // LSAPGPU_FILTER_FLAGS bit 0 one lane per warp after a CTA fence on every lane
-      mbar_init(&item_done[k], (st.filter_flags & 1) ? kFW : kFW * 32);
+      mbar_init(&item_done[k], kFW * 32);  // every consumer lane arrives (its own queue stores released)
       mbar_init(&queue_free[k], 1);
       qn[k] = 0;
       tmax[k] = kFNeg;
@@ -530,13 +528,7 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
       }
       // every lane arrives after its last use of row buffer rb and its own
       // queue stores: releases the row and hands the queue to the verifier
-      if (st.filter_flags & 1) {
-        __threadfence_block();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
-      } else {
-        mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
-      }
+      mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
     }
   }
   __syncthreads();
@@ -578,12 +570,11 @@ cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cuda
   return launch_pdl(k, dim3(p.ctas), dim3(32 * (W + 3)), p.smem, st, d.pdl, d, full, p.bufs, p.filter_queue);
 }
 
-// consumer geometry from the plan's thread count: 608 = 16 warps x 8
-// positions per lane, 992 = 28 warps x 4 (more warps to hide latency)
+// consumer geometry: 16 warps x 8 positions per lane (24 x 4 measured no
+// faster at C4 / C5: the kernel is not short of warps)
 template <class E, class Q, int RB>
 cudaError_t launch_filter_g(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  return p.threads == 32 * 27 ? launch_filter_t<E, Q, RB, 24, 4>(d, p, full, st)
-                              : launch_filter_t<E, Q, RB, 16, 8>(d, p, full, st);
+  return launch_filter_t<E, Q, RB, 16, 8>(d, p, full, st);
 }
 
 }  // namespace scan_detail

@@ -33,7 +33,6 @@ struct DevState {
   uint32_t* aux = nullptr;
   double qscale = 0.0;
   int filter_check = 0;  // > 0: the filter scan re-verifies every k-th item unfiltered (diagnostics)
-  int filter_flags = 0;  // filter scan variants under measurement (LSAPGPU_FILTER_FLAGS)
 
   double* agent_delta = nullptr;
   int32_t* agent_partner = nullptr;

@@ -40,6 +40,14 @@ mats = [
     # scale) smaller than the rest: the fused copies are redone separately
     ("probe-small", f32(rng.random((1500, 1500)) * np.where(np.arange(1500) < 64, 1e-3, 1.0)[:, None])),
     ("probe-large", f32(rng.random((1500, 1500)) * np.where(np.arange(1500) < 64, 1.0, 1e-3)[:, None])),
+    # every other storage type the filter serves when its rows are too long
+    # for the resident kernel: int16, int32, fp64 (exact copies of the values
+    # are verified; the quantized copies only filter)
+    ("int16", rng.integers(-30000, 30000, (1300, 1300)).astype(np.float64)),
+    ("int32", rng.integers(-5000000, 5000000, (1300, 1300)).astype(np.float64)),
+    ("fp64", o.generate("geom", 1400, 3)),
+    ("fp64-huge", rng.random((900, 900)) * 1e250),
+    ("int32-ties", rng.integers(0, 3, (1100, 1100)).astype(np.float64) * 70000),
 ]
 import torch
 for k, (name, a) in enumerate(mats):
