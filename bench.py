@@ -263,6 +263,8 @@ def sweep_block(g, args, wname: str, world: int, rank: int, local: int) -> dict:
     ctx = g.Context(local)
     exch = transport = None
     try:
+        if world > 1 and args.placement == "rows":
+            ctx.set_placement(rank, world)  # this rank's row block of A + all of AT
         ctx.generate(kind, n, iseed, param)
         if world > 1:
             exch, transport = _make_exchange(ctx, args)
@@ -299,6 +301,8 @@ def sweep_block(g, args, wname: str, world: int, rank: int, local: int) -> dict:
         return {
             "workload": desc, "n": n, "n_gpus": world, "ms": ms, "step_ms_all": times,
             "transport": transport if world > 1 else "none (one GPU)",
+            "placement": ("row blocks of A + AT replicated" if args.placement == "rows" else "full A + AT replicas")
+                         if world > 1 else "single",
             "full_sweep_ms": full_ms, "items_per_rank": own,
             "full_sweep_algorithmic_gbs": alg / (full_ms * 1e-3) / 1e9,
             "full_sweep_frac": alg / (full_ms * 1e-3) / 1e9 / pk,
@@ -346,6 +350,8 @@ def run_ours(args, wl) -> None:
     if world > 1 and not sharded:
         iseed = iseed + rank
     ctx = g.Context(local)
+    if sharded and args.placement == "rows":
+        ctx.set_placement(rank, world)
     cfg = g.ParallelConfig(seed=0)
     stream = torch.cuda.ExternalStream(ctx.stream)
     exch = None
@@ -548,8 +554,9 @@ def run_ours(args, wl) -> None:
         "data": "synthetic",
         "config": {"workload": desc, "n": n, "solver_seed": 0, "reeval": "touched_and_conflicted",
                    "storage": rep.gpu["storage"],
-                   "parallelism": (f"sharded x{world}: scan items by agent index, record exchange: {transport}, "
-                                   f"replicated commit" if sharded else
+                   "parallelism": (f"sharded x{world}: scan items by agent row block, "
+                                   f"{'A as row blocks + AT replicated' if args.placement == 'rows' else 'A + AT replicated'}, "
+                                   f"record exchange: {transport}, replicated commit" if sharded else
                                    f"replicas x{world}" if world > 1 else "single"),
                    "l2": "inputs larger than L2 (8*n^2 B fp64 source + A/AT), no flush needed",
                    "step": "device-resident fp64 input -> layout -> dgs_parallel (trace on) -> sigma/tau on host"},
@@ -581,6 +588,8 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent instances instead of one sharded solve")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 sharded: record exchange over peer memory (default) or an NCCL allgather")
+    ap.add_argument("--placement", default="rows", choices=["rows", "replicas"],
+                    help="N > 1 sharded: each rank holds its row block of A + all of AT (rows), or full replicas")
     ap.add_argument("--blocks", default="c4,c5",
                     help="comma list of BASELINE configs to also run sharded at this N (\"\" for none)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],

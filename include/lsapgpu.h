@@ -113,6 +113,16 @@ const char* lsapgpu_last_error(const lsapgpu_ctx* ctx);
 /* the stream all work of this context is ordered on (a cudaStream_t) */
 void* lsapgpu_stream(lsapgpu_ctx* ctx);
 
+/* Row-block placement for a multi-GPU solve (SURVEY §8(e) placement (i)):
+ * this context will hold rows [n*rank/world, n*(rank+1)/world) of A -- the
+ * agents this rank scans -- and all of AT (every other A[i][j] is read as
+ * AT[j][i]), instead of full replicas of both.  Call before setting the
+ * matrix; the matrix must then be solved with lsapgpu_solve_dist as that
+ * rank of that many (single-GPU entry points refuse it).  world = 1 (the
+ * default) holds every row.  Replaces nothing in the reference (its solver is
+ * one process); sized for n beyond one full A + AT replica per GPU. */
+int lsapgpu_set_placement(lsapgpu_ctx* ctx, int32_t rank, int32_t world);
+
 /* Instance upload.  `data` is a row-major n x n matrix of `dtype` in host
  * memory (pinned or pageable).  Validates n >= 1 and finiteness exactly like
  * Instance::validate, chooses the narrowest lossless device storage, and

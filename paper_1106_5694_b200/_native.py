@@ -27,6 +27,7 @@ EXPORTS = [
     "lsapgpu_evaluate_all", "lsapgpu_check_conflicts", "lsapgpu_apply_parallel_switches",
     "lsapgpu_random_perm", "lsapgpu_objective", "lsapgpu_counters", "lsapgpu_solve_dist",
     "lsapgpu_dist_exchange_bytes", "lsapgpu_set_scan_timing", "lsapgpu_scan_timing", "lsapgpu_scan_plan",
+    "lsapgpu_set_placement",
     "lsapgpu_set_timeline", "lsapgpu_timeline", "lsapgpu_auction_solve",
     "lsapgpu_greedy_assignment",
     "lsapgpu_dist_p2p_bytes", "lsapgpu_ipc_handle", "lsapgpu_ipc_open", "lsapgpu_ipc_close",
@@ -166,6 +167,7 @@ def _load() -> C.CDLL:
                                             vp, vp, i64]),
         "lsapgpu_greedy_assignment": (C.c_int, [vp, vp, C.POINTER(i64)]),
         "lsapgpu_scan_plan": (C.c_int, [vp, vp, C.c_int32]),
+        "lsapgpu_set_placement": (C.c_int, [vp, C.c_int32, C.c_int32]),
         "lsapgpu_scan_timing": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl),
                                           C.POINTER(i64), C.POINTER(dbl), C.POINTER(i64)]),
     }

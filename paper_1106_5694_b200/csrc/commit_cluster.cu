@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kNT, 1)
 
   Ctrl* C = st.ctrl;
   const int32_t n = st.n;
-  const E* A = static_cast<const E*>(st.A);
+  const E* AT = static_cast<const E*>(st.AT);  // A[i][j] = AT[j][i]: AT is whole on every rank
   E* acur = static_cast<E*>(st.acur);
   const int64_t ld = st.ld;
   // every control field in one round trip (independent loads: no dependent
@@ -435,9 +435,9 @@ __global__ void __launch_bounds__(kNT, 1)
       st.job_delta[j_new] = 0.0;
       st.job_partner[j_new] = -1;
     }
-    const int64_t ra = static_cast<int64_t>(agent) * ld, rd = static_cast<int64_t>(disp) * ld;
-    const auto a_new = widen(A[ra + j_new]), a_old = widen(A[ra + j_old]);
-    const auto d_old = widen(A[rd + j_old]), d_new = widen(A[rd + j_new]);
+    const int64_t rn = static_cast<int64_t>(j_new) * ld, ro = static_cast<int64_t>(j_old) * ld;
+    const auto a_new = widen(AT[rn + agent]), a_old = widen(AT[ro + agent]);
+    const auto d_old = widen(AT[ro + disp]), d_new = widen(AT[rn + disp]);
     const double dact = en.x < n ? static_cast<double>(delta4(a_new, a_old, d_old, d_new))
                                  : static_cast<double>(delta4(a_new, d_new, d_old, a_old));
     if (dact > eps) {

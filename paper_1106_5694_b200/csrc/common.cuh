@@ -154,9 +154,12 @@ __device__ __forceinline__ int4 prop_key(const Prop& p, int32_t n) {
   return p.slot < n ? make_int4(p.slot, p.a, p.j_new, p.j_old) : make_int4(p.slot, p.d, p.a, p.j_new);
 }
 
-// A[i][j] widened to fp64 for any storage type (exact)
-__device__ __forceinline__ double mat_at(const void* M, int storage, int64_t ld, int32_t i, int32_t j) {
-  const int64_t k = static_cast<int64_t>(i) * ld + j;
+// A[i][j] widened to fp64 for any storage type (exact), read from the
+// TRANSPOSE AT[j][i]: every rank holds all of AT, while A may be held as a
+// row block only (row-block placement)
+__device__ __forceinline__ double mat_at(const void* AT, int storage, int64_t ld, int32_t i, int32_t j) {
+  const int64_t k = static_cast<int64_t>(j) * ld + i;
+  const void* M = AT;
   switch (storage) {
     case kI16: return static_cast<double>(static_cast<const int16_t*>(M)[k]);
     case kI32: return static_cast<double>(static_cast<const int32_t*>(M)[k]);

@@ -1,6 +1,7 @@
 // dist.cu -- record exchange for the multi-GPU solve (placement
-// (ii)): every rank holds a full replica of A / AT, scans only the work items
-// it owns (agent i with i % world == rank), packs the records it produced, and
+// (ii), or (i) with A held as row blocks): every rank holds AT (and A or its
+// row block), scans only the work items it owns (the agents of its row block),
+// packs the records it produced, and
 // after the caller's allgather (NCCL over NVLink) every rank merges all ranks'
 // records into its tables and rebuilds the proposal list.  The commit kernel
 // then runs replicated: its result does not depend on proposal order, so all
@@ -26,13 +27,20 @@ struct Rec {
 static_assert(sizeof(Rec) == 32, "exchange record layout");
 
 // This rank's share of the work list (or of the identity list for a full sweep).
+// Items are owned by agent ROW BLOCKS: rank r scans agents
+// [floor(n r / w), floor(n (r+1) / w)) -- the rows of A it holds under the
+// row-block placement.
+__device__ __forceinline__ int32_t block_owner(int32_t a, int32_t n, int32_t world) {
+  return static_cast<int32_t>((static_cast<int64_t>(a + 1) * world - 1) / n);
+}
+
 __global__ void own_items_kernel(DevState st, int full, int32_t rank, int32_t world) {
   const int32_t n = st.n;
   const int32_t count = full ? n : st.ctrl->work_count;
   for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
     const uint32_t w = full ? (static_cast<uint32_t>(k) | kItemAgent | kItemJob) : st.items[k];
     const int32_t a = static_cast<int32_t>(w & kItemMask);
-    if (a % world != rank) continue;
+    if (block_owner(a, n, world) != rank) continue;
     const int pos = atomicAdd(&st.ctrl->own_count, 1);
     st.items_own[pos] = w;
   }
@@ -94,7 +102,7 @@ __device__ __forceinline__ void merge_body(const DevState& st, const unsigned ch
         st.agent_partner[i] = rec.agent_partner;
         if (rec.agent_partner >= 0) {
           const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
-          st.edges[P][pos] = agent_prop(st.sigma, st.tau, st.A, st.storage, st.ld, i, rec.agent_partner,
+          st.edges[P][pos] = agent_prop(st.sigma, st.tau, st.AT, st.storage, st.ld, i, rec.agent_partner,
                                         rec.agent_delta);
         }
       }
@@ -103,7 +111,7 @@ __device__ __forceinline__ void merge_body(const DevState& st, const unsigned ch
         st.job_partner[rec.job] = rec.job_partner;
         if (rec.job_partner >= 0) {
           const int pos = atomicAdd(&st.ctrl->edge_count[P], 1);
-          st.edges[P][pos] = job_prop(st.sigma, st.tau, st.A, st.storage, st.ld, n, rec.job, rec.job_partner,
+          st.edges[P][pos] = job_prop(st.sigma, st.tau, st.AT, st.storage, st.ld, n, rec.job, rec.job_partner,
                                       rec.job_delta);
         }
       }

@@ -32,6 +32,11 @@ __device__ __forceinline__ double unit_double(uint64_t u) {
 struct Src {
   LayoutSource s;
   int32_t n;
+  // row-block placement: does this rank hold row i of A, and where
+  __device__ __forceinline__ bool own(int64_t i) const {
+    return s.a_rows < 0 || (i >= s.a_row0 && i < static_cast<int64_t>(s.a_row0) + s.a_rows);
+  }
+  __device__ __forceinline__ int64_t local(int64_t i) const { return s.a_rows < 0 ? i : i - s.a_row0; }
   __device__ __forceinline__ double operator()(int64_t i, int64_t j) const {
     const int64_t k = i * n + j;
     switch (s.kind) {
@@ -151,7 +156,7 @@ __global__ void build_layout_kernel(Src src, int64_t row0, int64_t rows, E* A, E
     const int64_t i = bi + r, j = bj + threadIdx.x;
     if (i < rend && j < n) {
       const E v = narrow<E>(src(i, j));
-      A[i * ld + j] = v;
+      if (src.own(i)) A[src.local(i) * ld + j] = v;
       tile[r][threadIdx.x] = v;
     }
   }
@@ -256,13 +261,16 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
       if (j + 1 < n && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
     }
     const E e0 = narrow<E>(isfinite(v0) ? v0 : 0.0), e1 = narrow<E>(isfinite(v1) ? v1 : 0.0);
-    if (j + 1 < n)
-      Pair<E>::st(A + i * ld + j, e0, e1);
-    else if (j < n)
-      A[i * ld + j] = e0;
+    const bool own = src.own(i);  // row-block placement: A / Q rows of this rank only
+    const int64_t li = src.local(i);
+    if (own && j + 1 < n)
+      Pair<E>::st(A + li * ld + j, e0, e1);
+    else if (own && j < n)
+      A[li * ld + j] = e0;
     tile[r][2 * lane] = e0;
     tile[r][2 * lane + 1] = e1;
-    if (qt.bits && j < n) qstore_pair(qt, i * ld + j, static_cast<double>(e0), static_cast<double>(e1), j + 1 < n);
+    if (qt.bits && own && j < n)
+      qstore_pair(qt, li * ld + j, static_cast<double>(e0), static_cast<double>(e1), j + 1 < n);
   }
   __syncthreads();
   // AT rows bj .. bj+63, columns (agents) bi .. bi+63
@@ -338,20 +346,20 @@ template <class E>
 __global__ void init_assignment_kernel(DevState d) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.n) return;
-  const E* A = static_cast<const E*>(d.A);
+  const E* AT = static_cast<const E*>(d.AT);  // A[i][j] = AT[j][i] (A may be a row block)
   const int32_t i = d.sigma[j];
   d.tau[i] = j;
   if (d.tau16) d.tau16[i] = static_cast<uint16_t>(j);
-  static_cast<E*>(d.acur)[i] = A[static_cast<int64_t>(i) * d.ld + j];
+  static_cast<E*>(d.acur)[i] = AT[static_cast<int64_t>(j) * d.ld + i];
 }
 
 template <class E>
 __global__ void gather_current_kernel(DevState d, double* out, int pack) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.n) return;
-  const E* A = static_cast<const E*>(d.A);
+  const E* AT = static_cast<const E*>(d.AT);
   const int32_t sj = d.sigma[j];
-  out[j] = static_cast<double>(A[static_cast<int64_t>(sj) * d.ld + j]);
+  out[j] = static_cast<double>(AT[static_cast<int64_t>(j) * d.ld + sj]);
   if (pack) {  // [values | sigma | tau] for one device->host copy
     int32_t* w = reinterpret_cast<int32_t*>(out + d.n);
     w[j] = sj;
@@ -361,11 +369,11 @@ __global__ void gather_current_kernel(DevState d, double* out, int pack) {
 
 template <class E>
 __global__ void read_rows_kernel(DevState d, const int32_t* rows, int32_t nrows, double* out) {
-  const E* A = static_cast<const E*>(d.A);
+  const E* AT = static_cast<const E*>(d.AT);  // (A may be a row block; AT is whole)
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
        k < static_cast<int64_t>(nrows) * d.n; k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = k / d.n, j = k % d.n;
-    out[k] = static_cast<double>(A[static_cast<int64_t>(rows[r]) * d.ld + j]);
+    out[k] = static_cast<double>(AT[j * d.ld + rows[r]]);
   }
 }
 
@@ -463,8 +471,9 @@ cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, 
 
 cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(d.n) * d.ld;
+  const int64_t a_total = static_cast<int64_t>(d.a_rows) * d.ld;  // A / Q: this rank's row block
   const dim3 g(148 * 8), b(256);
-  cudaError_t e = dispatch<QuantK>(d.storage, g, b, st, d.A, Q, total, d.n, d.ld, scale, qbits);
+  cudaError_t e = dispatch<QuantK>(d.storage, g, b, st, d.A, Q, a_total, d.n, d.ld, scale, qbits);
   if (e != cudaSuccess) return e;
   return dispatch<QuantK>(d.storage, g, b, st, d.AT, QT, total, d.n, d.ld, scale, qbits);
 }

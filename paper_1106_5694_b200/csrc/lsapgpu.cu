@@ -162,6 +162,7 @@ struct lsapgpu_ctx {
   std::vector<Buf> vec_bufs;
   Buf mat;                // A and AT (one allocation)
   Buf qmat;               // Q and QT: quantized filter copies (scan_filter.cuh), when the plan uses them
+  int32_t place_rank = 0, place_world = 1;  // row-block placement of A (lsapgpu_set_placement)
   int quant_bits = 0;     // copies the last layout pass wrote (0: none) and their scale
   double quant_scale = 0.0;
   bool quant_fused = false;  // the current copies came from the layout pass (no quantize pass)
@@ -368,21 +369,48 @@ int storage_of_flags(uint32_t flags) {
 }
 
 // (Re)points A/AT at an allocation large enough for n x ld elements of `storage`.
+// Rows of A this context holds: all, or under the row-block placement
+// (lsapgpu_set_placement) the block of rank `rank` of `world`.
+void placement_rows(const lsapgpu_ctx* ctx, int32_t n, int32_t* row0, int32_t* rows) {
+  const int64_t r = ctx->place_rank, w = ctx->place_world;
+  *row0 = static_cast<int32_t>(n * r / w);
+  *rows = static_cast<int32_t>(n * (r + 1) / w) - *row0;
+}
+
 int alloc_matrix(lsapgpu_ctx* ctx, int32_t n, int storage) {
   const int64_t ld = pitch_of(n);
-  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(ld) * esize(storage);
-  if (ctx->mat.bytes < 2 * bytes) {
+  int32_t row0 = 0, rows = n;
+  placement_rows(ctx, n, &row0, &rows);
+  const size_t at_bytes = static_cast<size_t>(n) * static_cast<size_t>(ld) * esize(storage);
+  const size_t a_bytes = (static_cast<size_t>(rows) * static_cast<size_t>(ld) * esize(storage) + 255) / 256 * 256;
+  if (ctx->mat.bytes < a_bytes + at_bytes) {
     if (ctx->mat.p) cudaFree(ctx->mat.p);
     ctx->mat.p = nullptr;
     ctx->mat.bytes = 0;
-    CK(cudaMalloc(&ctx->mat.p, 2 * bytes));
-    ctx->mat.bytes = 2 * bytes;
+    CK(cudaMalloc(&ctx->mat.p, a_bytes + at_bytes));
+    ctx->mat.bytes = a_bytes + at_bytes;
   }
   DevState& d = ctx->d;
   d.storage = storage;
   d.A = ctx->mat.p;
-  d.AT = static_cast<unsigned char*>(ctx->mat.p) + bytes;
+  d.AT = static_cast<unsigned char*>(ctx->mat.p) + a_bytes;
+  d.a_row0 = row0;
+  d.a_rows = rows;
   return LSAPGPU_OK;
+}
+
+// Single-GPU entry points need every row of A: refuse a row-block context.
+int require_full_rows(lsapgpu_ctx* ctx, const char* what) {
+  if (ctx->place_world <= 1) return LSAPGPU_OK;
+  return fail(ctx, LSAPGPU_ERR_STATE,
+              std::string(what) + ": this context holds a row block of the matrix (lsapgpu_set_placement); "
+                                  "only the multi-GPU solve of its rank can use it");
+}
+
+// the layout source's share of A for this context (all rows: -1)
+void set_source_rows(const lsapgpu_ctx* ctx, LayoutSource* src) {
+  src->a_row0 = ctx->d.a_row0;
+  src->a_rows = ctx->d.a_rows == ctx->d.n ? -1 : ctx->d.a_rows;
 }
 
 // Quantized filter copies for the long-row scan (scan_filter.cuh): a
@@ -402,16 +430,18 @@ double quant_scale_for(float amax, int bits) {
 
 int alloc_quant(lsapgpu_ctx* ctx, int bits, void** Q, void** QT) {
   const DevState& d = ctx->d;
-  const size_t bytes = static_cast<size_t>(d.n) * static_cast<size_t>(d.ld) * static_cast<size_t>(bits / 8);
-  if (ctx->qmat.bytes < 2 * bytes) {
+  const size_t qt_bytes = static_cast<size_t>(d.n) * static_cast<size_t>(d.ld) * static_cast<size_t>(bits / 8);
+  const size_t q_bytes =  // Q: this context's row block of A
+      (static_cast<size_t>(d.a_rows) * static_cast<size_t>(d.ld) * static_cast<size_t>(bits / 8) + 255) / 256 * 256;
+  if (ctx->qmat.bytes < q_bytes + qt_bytes) {
     if (ctx->qmat.p) cudaFree(ctx->qmat.p);
     ctx->qmat.p = nullptr;
     ctx->qmat.bytes = 0;
-    CK(cudaMalloc(&ctx->qmat.p, 2 * bytes));
-    ctx->qmat.bytes = 2 * bytes;
+    CK(cudaMalloc(&ctx->qmat.p, q_bytes + qt_bytes));
+    ctx->qmat.bytes = q_bytes + qt_bytes;
   }
   *Q = ctx->qmat.p;
-  *QT = static_cast<unsigned char*>(ctx->qmat.p) + bytes;
+  *QT = static_cast<unsigned char*>(ctx->qmat.p) + q_bytes;
   return LSAPGPU_OK;
 }
 
@@ -514,6 +544,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
   const int spec = storage_of_flags(flags);
   if ((rc = alloc_matrix(ctx, n, spec))) return rc;
+  set_source_rows(ctx, &src);
   DevState& d = ctx->d;
   QuantTarget qt;
   if ((rc = prepare_quant(ctx, spec, bits_to_float(fl4[3]), &qt))) return rc;
@@ -527,6 +558,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   if (storage != spec) {
     ctx->quant_bits = 0;
     if ((rc = alloc_matrix(ctx, n, storage))) return rc;
+    set_source_rows(ctx, &src);
     CK(launch_build_layout(src, n, 0, n, storage, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
                            ctx->stream));
     ++ctx->launches;
@@ -620,6 +652,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   src.kind = 0;
   src.src = ctx->stage.p;
   src.src_dtype = ndtype;
+  set_source_rows(ctx, &src);
   const int T_ = ctx->pool->size();
   std::vector<uint8_t> okv(static_cast<size_t>(T_));
   for (int k = 0; k < nchunks; ++k) {
@@ -658,6 +691,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     ctx->quant_bits = 0;
     int rc = alloc_matrix(ctx, n, final_storage);
     if (rc) return rc;
+    set_source_rows(ctx, &src);
     CK(launch_build_layout(src, n, 0, n, final_storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
                            ctx->d.ld, ctx->stream));
     ++ctx->launches;
@@ -798,6 +832,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
         cudaStreamSynchronize(ctx->copy_stream);
         return rc;
       }
+      set_source_rows(ctx, &src);
     }
     CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
                            const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->chunk_flags + k, ctx->stream,
@@ -814,6 +849,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
   if (final_storage != storage) {  // a later chunk needs a wider type: rebuild everything
     ctx->quant_bits = 0;
     if ((rc = alloc_matrix(ctx, n, final_storage))) return rc;
+    set_source_rows(ctx, &src);
     CK(launch_build_layout(src, n, 0, n, final_storage, const_cast<void*>(ctx->d.A),
                            const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->stream));
     ++ctx->launches;
@@ -1112,6 +1148,18 @@ void* lsapgpu_stream(lsapgpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st
 int32_t lsapgpu_n(const lsapgpu_ctx* ctx) { return ctx ? ctx->n_matrix : 0; }
 int32_t lsapgpu_storage(const lsapgpu_ctx* ctx) { return ctx && ctx->n_matrix ? ctx->d.storage : -1; }
 
+int lsapgpu_set_placement(lsapgpu_ctx* ctx, int32_t rank, int32_t world) {
+  if (!ctx) return LSAPGPU_ERR_INVALID;
+  if (world < 1 || rank < 0 || rank >= world) return fail(ctx, LSAPGPU_ERR_INVALID, "invalid rank / world");
+  if (ctx->place_rank != rank || ctx->place_world != world) {
+    ctx->place_rank = rank;
+    ctx->place_world = world;
+    ctx->n_matrix = 0;  // the layout depends on it: set the matrix again
+    drop_graph(ctx);
+  }
+  return LSAPGPU_OK;
+}
+
 int lsapgpu_set_matrix_device(lsapgpu_ctx* ctx, const void* dev_data, int32_t n, int32_t dtype) {
   if (!ctx) return LSAPGPU_ERR_INVALID;
   CK(cudaSetDevice(ctx->device));
@@ -1271,6 +1319,7 @@ int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launc
 int lsapgpu_evaluate_all(lsapgpu_ctx* ctx, const int32_t* sigma, double eps, double* agent_delta,
                          int32_t* agent_partner, double* job_delta, int32_t* job_partner) {
   if (!ctx || !ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
+  if (int rc = require_full_rows(ctx, "evaluate_all_parallel")) return rc;
   CK(cudaSetDevice(ctx->device));
   if (!(eps >= 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "improvement_epsilon must be >= 0");
   const int32_t n = ctx->n_matrix;
@@ -1370,6 +1419,7 @@ int lsapgpu_apply_parallel_switches(lsapgpu_ctx* ctx, int32_t* sigma, int32_t* t
                                     double eps, int32_t* applied_agent, int32_t* applied_new_job,
                                     int32_t* applied_old_job, int32_t* applied_displaced,
                                     double* applied_delta, int32_t* n_applied) {
+  if (ctx && ctx->n_matrix && ctx->place_world > 1) return require_full_rows(ctx, "apply_parallel_switches");
   if (!ctx || !ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
   CK(cudaSetDevice(ctx->device));
   if (!(eps >= 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "improvement_epsilon must be >= 0");
@@ -1484,6 +1534,12 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   if (multi && !p2p && (!dist->allgather || !dist->send_dev || !dist->recv_dev))
     return fail(ctx, LSAPGPU_ERR_INVALID, "multi-GPU solve needs an allgather callback and exchange buffers");
   if (p2p && dist->world > kMaxPeers) return fail(ctx, LSAPGPU_ERR_INVALID, "peer transport: at most 8 ranks");
+  if (ctx->place_world > 1 && !(multi && dist->world == ctx->place_world && dist->rank == ctx->place_rank))
+    return fail(ctx, LSAPGPU_ERR_STATE,
+                "this context holds row block " + std::to_string(ctx->place_rank) + " of " +
+                    std::to_string(ctx->place_world) + " of the matrix: solve it as that rank of that many");
+  if (ctx->place_world > 1 && params->init_mode == LSAPGPU_INIT_GREEDY)
+    return fail(ctx, LSAPGPU_ERR_STATE, "the greedy start needs every row of A (full replicas)");
   const size_t xbytes = multi ? dist_exchange_bytes(n, dist->world) : 0;
   PeerSet ps{};
   if (p2p) {
@@ -1858,6 +1914,7 @@ int lsapgpu_auction_solve(lsapgpu_ctx* ctx, const lsapgpu_auction_params* params
   if (!ctx) return LSAPGPU_ERR_INVALID;
   if (!ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
   if (!params || !sigma_out) return fail(ctx, LSAPGPU_ERR_INVALID, "null argument");
+  if (int rc = require_full_rows(ctx, "auction_solve")) return rc;
   const lsapgpu_auction_params& P = *params;
   // AuctionConfig::validate (baselines.hpp:22-25)
   if (P.has_epsilon && !(P.epsilon > 0.0)) return fail(ctx, LSAPGPU_ERR_INVALID, "auction: epsilon must be > 0");
@@ -1987,6 +2044,7 @@ int lsapgpu_greedy_assignment(lsapgpu_ctx* ctx, int32_t* sigma_out, int64_t* rou
   if (!ctx) return LSAPGPU_ERR_INVALID;
   if (!ctx->n_matrix) return fail(ctx, LSAPGPU_ERR_STATE, "no matrix set");
   if (!sigma_out) return fail(ctx, LSAPGPU_ERR_INVALID, "null argument");
+  if (int rc0 = require_full_rows(ctx, "greedy_assignment")) return rc0;
   CK(cudaSetDevice(ctx->device));
   int rc = run_greedy(ctx);
   if (rc) return rc;

@@ -135,10 +135,11 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int32_t n = st.n;
   const int64_t ld = st.ld;
-  const Q* __restrict__ Qg = static_cast<const Q*>(st.Q);
+  // this rank's row blocks of Q and A (row-block placement; single GPU: all rows)
+  const Q* __restrict__ Qg = static_cast<const Q*>(st.Q) - static_cast<int64_t>(st.a_row0) * st.ld;
   const Q* __restrict__ QTg = static_cast<const Q*>(st.QT);
   const uint32_t* __restrict__ aux_g = st.aux;
-  const E* __restrict__ A = static_cast<const E*>(st.A);
+  const E* __restrict__ A = static_cast<const E*>(st.A) - static_cast<int64_t>(st.a_row0) * st.ld;
   const E* __restrict__ AT = static_cast<const E*>(st.AT);
   const E* __restrict__ acur_g = static_cast<const E*>(st.acur);
   const int32_t* __restrict__ tau_g = st.tau;
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
             ebuf[pos] = entry;
           } else {
             const int gg = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
-            st.edges[parity_out][gg] = finish_prop(entry, st.sigma, tau_g, st.A, st.storage, ld, n);
+            st.edges[parity_out][gg] = finish_prop(entry, st.sigma, tau_g, st.AT, st.storage, ld, n);
           }
         }
         __syncwarp();
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
   if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
   __syncthreads();
   for (int e = tid; e < ne; e += kFThreads)
-    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.A, st.storage, ld, n);
+    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.AT, st.storage, ld, n);
 }
 
 // Per-launch position array: aux[p] = tau[p] * sizeof(Q) | (floor(acur[p] * S) + 2^14) << 17

@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int32_t n = st.n;
   const int64_t ld = st.ld;
-  const E* __restrict__ A = static_cast<const E*>(st.A);
+  const E* __restrict__ A = static_cast<const E*>(st.A) - static_cast<int64_t>(st.a_row0) * st.ld;  // own row block
   const E* __restrict__ AT = static_cast<const E*>(st.AT);
   const E* __restrict__ acur = static_cast<const E*>(st.acur);
   const int32_t* __restrict__ tau = st.tau;
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
                 ebuf[pos] = entry;
               } else {  // overflow: direct global append
                 const int g = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
-                st.edges[parity_out][g] = finish_prop(entry, st.sigma, tau, st.A, st.storage, ld, n);
+                st.edges[parity_out][g] = finish_prop(entry, st.sigma, tau, st.AT, st.storage, ld, n);
               }
             }
           }
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) pair_scan_kernel(DevState st, in
   if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
   __syncthreads();
   for (int e = tid; e < ne; e += NT)
-    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau, st.A, st.storage, ld, n);
+    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau, st.AT, st.storage, ld, n);
 }
 
 constexpr size_t kStaticSmem = 14 * 1024;  // ebuf + item metadata + counters (+ slack)

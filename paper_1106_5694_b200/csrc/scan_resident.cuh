@@ -146,7 +146,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int32_t n = st.n;
   const int64_t ld = st.ld;
-  const E* __restrict__ A = static_cast<const E*>(st.A);
+  // this rank's rows of A (row-block placement: rows a_row0.. are held; the
+  // scans only ever touch the rows of the items this rank owns)
+  const E* __restrict__ A = static_cast<const E*>(st.A) - static_cast<int64_t>(st.a_row0) * st.ld;
   const E* __restrict__ AT = static_cast<const E*>(st.AT);
   const E* __restrict__ acur_g = static_cast<const E*>(st.acur);
   const int32_t* __restrict__ tau_g = st.tau;
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                 ebuf[pos] = entry;
               } else {  // overflow: direct global append
                 const int g = atomicAdd(&st.ctrl->edge_count[parity_out], 1);
-                st.edges[parity_out][g] = finish_prop(entry, st.sigma, tau_g, st.A, st.storage, ld, n);
+                st.edges[parity_out][g] = finish_prop(entry, st.sigma, tau_g, st.AT, st.storage, ld, n);
               }
             }
           }
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
   if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
   __syncthreads();
   for (int e = tid; e < ne; e += kResThreads)
-    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.A, st.storage, ld, n);
+    st.edges[parity_out][gbase + e] = finish_prop(ebuf[e], st.sigma, tau_g, st.AT, st.storage, ld, n);
   if (st.tl_cap > 8192) {  // per-CTA end stamps (deep instrumentation only)
     __syncthreads();
     if (tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, stages > 1 ? 12 : 11);

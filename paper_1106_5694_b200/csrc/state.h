@@ -21,6 +21,11 @@ struct DevState {
   int storage = kF64;
   const void* A = nullptr;   // row-major, n x ld
   const void* AT = nullptr;  // transposed, n x ld
+  // row-block placement (multi-GPU): this rank holds rows
+  // [a_row0, a_row0 + a_rows) of A (and of Q) -- the agents it scans -- and
+  // all of AT; every other A[i][j] is read as AT[j][i].  Single GPU: 0, n.
+  int32_t a_row0 = 0;
+  int32_t a_rows = 0;
   int32_t* sigma = nullptr;  // job -> agent (padded to ld)
   int32_t* tau = nullptr;    // agent -> job (padded to ld)
   uint16_t* tau16 = nullptr; // the same as uint16 when n < 65536 (the resident scan bulk-loads it)
@@ -101,6 +106,10 @@ struct LayoutSource {
   uint64_t seed = 0;
   double param = 0.0;
   const double* aux = nullptr;  // generator side tables (p2p: up,x,y; geom: xs,ys)
+  // row-block placement: write only rows [a_row0, a_row0 + a_rows) of A (and
+  // Q), at local row index i - a_row0; AT (and QT) whole.  a_rows < 0: all rows.
+  int32_t a_row0 = 0;
+  int32_t a_rows = -1;
 };
 // flags bit0: non-finite present, bit1: not int16-exact, bit2: not int32 (<2^29) exact,
 // bit3: not fp32-exact.

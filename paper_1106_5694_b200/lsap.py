@@ -601,6 +601,12 @@ class Context:
         return {"scan_ms": tot.value, "scan_launches": la.value, "full_ms": fl.value,
                 "full_launches": fla.value, "commit_ms": cm.value, "commit_launches": cl.value}
 
+    def set_placement(self, rank: int, world: int) -> None:
+        """Row-block placement (lsapgpu_set_placement): hold only rank's row
+        block of A (plus all of AT) for the multi-GPU solve; set before the
+        matrix."""
+        self._check(N.LIB.lsapgpu_set_placement(self.h, int(rank), int(world)))
+
     def scan_plan(self) -> dict:
         """The pair-scan plan chosen for the current matrix (lsapgpu_scan_plan)."""
         info = np.zeros(16, np.int32)

@@ -267,3 +267,53 @@ def test_sharded_large_filter_equals_single_gpu(tmp_path):
     assert out["plan"]["kernel"] == "filter" and out["plan"]["filter"] == 8
     assert out["ranks"] == [out["ref"], out["ref"]]
     assert out["values"] == [out["value"], out["value"]]
+
+
+@pytest.mark.parametrize("kind,n,world,peer,graph", [
+    ("p2p", 1500, 2, True, True),      # resident scan
+    ("int", 997, 3, False, False),     # ragged blocks, allgather transport, host-stepped
+    ("f32", 12000, 2, True, True),     # filter scan on the row block's Q rows
+    ("geom", 700, 4, True, False),     # fp64
+])
+def test_row_block_placement_equals_single_gpu(oracle, gpu_ctx, kind, n, world, peer, graph):
+    """Row-block placement (lsapgpu_set_placement, SURVEY §8(e) placement
+    (i)): each rank holds only its agents' rows of A (and Q) plus all of AT;
+    every rank returns the single-GPU result bit for bit, and single-GPU entry
+    points refuse such a context."""
+    import paper_1106_5694_b200 as g
+    from paper_1106_5694_b200.dist import ThreadExchange, ThreadPeerExchange
+    a = oracle.generate(kind, n, 8)
+    cfg = g.ParallelConfig(seed=2, use_graph=graph)
+    gpu_ctx.set_matrix(a)
+    ref = gpu_ctx.solve(cfg)
+    ex = (ThreadPeerExchange if peer else ThreadExchange).group(world)
+    out, errs = [None] * world, []
+
+    def run(r):
+        try:
+            ctx = g.Context(0)
+            ctx.set_placement(r, world)
+            ctx.set_matrix(a)
+            out[r] = [ctx.solve(cfg, dist=ex[r]) for _ in range(2)]
+            with pytest.raises(g.Error, match="row block"):
+                ctx.solve(cfg)
+            ctx.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            ex[r].shared["barrier"].abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    if peer:
+        for e in ex:
+            e.free()
+    if errs:
+        raise errs[0]
+    for reps in out:
+        for rep in reps:
+            assert np.array_equal(rep.assignment.sigma, ref.assignment.sigma)
+            assert rep.assignment.value == ref.assignment.value
+            assert rep.objective_trace == ref.objective_trace
