@@ -469,6 +469,30 @@ cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, 
   return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags, amax, qt);
 }
 
+// max |a| over the stored matrix (AT: whole on every rank), float bits rounded up
+template <class E>
+__global__ void amax_kernel(const E* __restrict__ AT, int32_t n, int64_t ld, uint32_t* out) {
+  float m = 0.f;
+  const int64_t total = static_cast<int64_t>(n) * ld;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (k % ld < n) m = fmaxf(m, __double2float_ru(fabs(static_cast<double>(AT[k]))));
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_down_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+template <class E>
+struct AmaxK {
+  static void run(dim3 g, dim3 b, cudaStream_t st, const void* AT, int32_t n, int64_t ld, uint32_t* out) {
+    amax_kernel<E><<<g, b, 0, st>>>(static_cast<const E*>(AT), n, ld, out);
+  }
+};
+
+cudaError_t launch_amax(const DevState& d, uint32_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  return dispatch<AmaxK>(d.storage, dim3(148 * 8), dim3(256), st, d.AT, d.n, d.ld, out);
+}
+
 cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(d.n) * d.ld;
   const int64_t a_total = static_cast<int64_t>(d.a_rows) * d.ld;  // A / Q: this rank's row block

@@ -479,6 +479,10 @@ int prepare_quant(lsapgpu_ctx* ctx, int storage, float probe_amax, QuantTarget* 
 int build_filter_copies(lsapgpu_ctx* ctx) {
   DevState& d = ctx->d;
   const ScanPlan& p = ctx->scan_plan;
+  if (!ctx->quant_bits) {  // the layout pass did not reduce max|a| (no copies planned then): do it now
+    CK(launch_amax(d, ctx->flags_dev + 2, ctx->stream));
+    ++ctx->launches;
+  }
   uint32_t bits = 0;
   CK(cpy(ctx, &bits, ctx->flags_dev + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -549,7 +553,7 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   QuantTarget qt;
   if ((rc = prepare_quant(ctx, spec, bits_to_float(fl4[3]), &qt))) return rc;
   CK(launch_layout_fused(src, n, 0, n, spec, const_cast<void*>(d.A), const_cast<void*>(d.AT), d.ld,
-                         ctx->flags_dev + 1, ctx->stream, ctx->flags_dev + 2, qt));
+                         ctx->flags_dev + 1, ctx->stream, qt.bits ? ctx->flags_dev + 2 : nullptr, qt));
   ++ctx->launches;
   CK(cpy(ctx, &flags, ctx->flags_dev + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -678,7 +682,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     CK(cudaEventRecord(ctx->ev_chunk[b], ctx->copy_stream));
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_chunk[b], 0));
     CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
-                           ctx->d.ld, ctx->chunk_flags + k, ctx->stream, ctx->flags_dev + 2, qt));
+                           ctx->d.ld, ctx->chunk_flags + k, ctx->stream, qt.bits ? ctx->flags_dev + 2 : nullptr, qt));
     ++ctx->launches;
   }
   std::vector<uint32_t> fl(nchunks);
@@ -836,7 +840,7 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
     }
     CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A),
                            const_cast<void*>(ctx->d.AT), ctx->d.ld, ctx->chunk_flags + k, ctx->stream,
-                           ctx->flags_dev + 2, qt));
+                           qt.bits ? ctx->flags_dev + 2 : nullptr, qt));
     ++ctx->launches;
   }
   std::vector<uint32_t> fl(nchunks);

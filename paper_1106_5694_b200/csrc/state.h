@@ -132,6 +132,8 @@ cudaError_t launch_gen_aux(const LayoutSource& s, int32_t n, double* aux, cudaSt
 cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, int64_t rows, int storage,
                                 void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st,
                                 uint32_t* amax = nullptr, QuantTarget qt = QuantTarget{});
+// max |entry| of the stored matrix as float bits rounded up, into *out
+cudaError_t launch_amax(const DevState& d, uint32_t* out, cudaStream_t st);
 // Q = ceil(A * scale), QT = ceil(AT * scale) as int16 (qbits 16) or int8 (qbits 8), padding zeroed
 cudaError_t launch_quantize(const DevState& d, int qbits, double scale, void* Q, void* QT, cudaStream_t st);
 cudaError_t launch_init_assignment(const DevState& d, cudaStream_t st);  // tau, acur from sigma

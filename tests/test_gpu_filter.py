@@ -94,6 +94,28 @@ def test_filter_is_the_default_long_row_scan(gpu_ctx):
     assert plan["filter"] == 16 and plan["m"] == 2, plan
 
 
+def test_filter_after_storage_misspeculation(gpu_ctx):
+    """The upload probe sees integer rows (int16 storage: resident kernel,
+    no quantized copies planned, max|a| not reduced in the layout pass); the
+    rest is fractional, so the matrix is rebuilt as fp32 with the filter
+    plan, whose scale then comes from a separate max|a| reduction."""
+    import numpy as np
+    from oracle.oracle import Oracle
+    o = Oracle()
+    rng = np.random.default_rng(5)
+    n = 12000
+    a = np.asarray(rng.random((n, n)) * 900.0, np.float32).astype(np.float64)
+    a[:64] = np.floor(a[:64] / 8.0)
+    gpu_ctx.set_matrix(a)
+    assert gpu_ctx.scan_plan()["filter"] in (8, 16), gpu_ctx.scan_plan()
+    s = o.random_perm(n, 1)
+    t = gpu_ctx.evaluate_all(s, 0.0)
+    ad, ap, jd, jp = o.evaluate_all(a, s, 0.0)
+    assert np.array_equal(t.agent_partner, ap) and np.array_equal(t.job_partner, jp)
+    assert np.array_equal(t.agent_delta.view(np.uint64), ad.view(np.uint64))
+    assert np.array_equal(t.job_delta.view(np.uint64), jd.view(np.uint64))
+
+
 LARGE = r'''
 import sys, json, hashlib; sys.path.insert(0, %r)
 import numpy as np
