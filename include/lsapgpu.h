@@ -102,6 +102,8 @@ typedef struct {
   int32_t scan_filter;        /* 0, or 8 / 16: the long-row scan's quantized filter copies */
   int64_t filter_kept;        /* filter scan: candidates verified exactly (all items of the solve) */
   int64_t filter_overflows;   /* filter scan: items verified by a whole-row exact scan (queue overflow) */
+  int64_t host_log_orders;    /* passes whose delta log the host had to put in batch order itself
+                                 (0 normally: the device orders it, log_order.cu) */
 } lsapgpu_stats;
 
 const char* lsapgpu_version(void);

@@ -103,8 +103,14 @@ inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {})
   rep.assignment.tau.resize(n);
   lsapgpu_stats st{};
   std::int64_t cap = 100000 + 4096;
-  std::vector<std::int64_t> ts(cap);
-  std::vector<double> tv(cap);
+  // per-thread scratch the library writes the trace into (kept: fresh
+  // buffers cost page faults and zeroing on every call)
+  static thread_local std::vector<std::int64_t> ts;
+  static thread_local std::vector<double> tv;
+  if (static_cast<std::int64_t>(ts.size()) < cap) {
+    ts.resize(static_cast<std::size_t>(cap));
+    tv.resize(static_cast<std::size_t>(cap));
+  }
   std::int64_t tl = 0;
   ctx.check(lsapgpu_solve(ctx.get(), &p, rep.assignment.sigma.data(), rep.assignment.tau.data(), &st,
                           ts.data(), tv.data(), cap, &tl));
@@ -113,8 +119,8 @@ inline SolveReport dgs_parallel(const Instance& inst, const GpuConfig& cfg = {})
     // 100000 cap (parallel.cpp:15-20,343-344): re-run with room for all of it
     // (the solve is deterministic without a deadline)
     cap = tl;
-    ts.assign(cap, 0);
-    tv.assign(cap, 0.0);
+    ts.resize(static_cast<std::size_t>(cap));
+    tv.resize(static_cast<std::size_t>(cap));
     ctx.check(lsapgpu_solve(ctx.get(), &p, rep.assignment.sigma.data(), rep.assignment.tau.data(), &st,
                             ts.data(), tv.data(), cap, &tl));
   }

@@ -66,6 +66,7 @@ class Stats(C.Structure):
         ("scan_filter", C.c_int32),
         ("filter_kept", C.c_int64),
         ("filter_overflows", C.c_int64),
+        ("host_log_orders", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

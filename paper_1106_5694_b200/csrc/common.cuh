@@ -105,8 +105,9 @@ struct Ctrl {
   // commit_apply): committed / queued-conflicted proposal lists of one batch
   int32_t k2_parity, k2_nlog, k2_nconf, k2_iter;
   int64_t k2_log_base;
-  // grid barrier of the resident scan when it runs the batch's apply itself
-  uint32_t gbar_count, gbar_gen;
+  // device ordering of the delta log (log_order.cu): nonzero if the log was
+  // not iteration-grouped with distinct slots per iteration; entries placed
+  uint32_t order_bad, order_total;
   uint32_t push_done;  // CTAs finished with the peer push of the current round
   uint32_t pad2_;
   uint64_t p2p_epoch;  // peer transport: rounds pushed (flags carry it; graph-capturable)

@@ -10,12 +10,20 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 
 namespace lsapgpu {
 
 namespace {
 
 constexpr double kF32Max = 3.4028234663852886e38;
+
+// streaming stores (default) or plain stores (LSAPGPU_NARROW_NT=0: the ring
+// slot stays in the cache hierarchy for the DMA engine to read)
+bool use_nt() {
+  static const bool v = !(std::getenv("LSAPGPU_NARROW_NT") && std::atoi(std::getenv("LSAPGPU_NARROW_NT")) == 0);
+  return v;
+}
 
 template <class T>
 bool narrow_scalar(const double* __restrict__ src, T* __restrict__ dst, size_t cnt, double lim) {
@@ -44,7 +52,7 @@ __attribute__((target("avx2"))) bool narrow_int_avx2(const double* __restrict__ 
   const __m256d hi = _mm256_set1_pd(lim), lo = _mm256_set1_pd(-lim);
   __m256d ok = _mm256_castsi256_pd(_mm256_set1_epi64x(-1));
   size_t i = 0;
-  const bool nt = (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (8 * sizeof(T)) % 16 == 0;
+  const bool nt = use_nt() && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (8 * sizeof(T)) % 16 == 0;
   for (; i + 8 <= cnt; i += 8) {
     const __m256d v0 = _mm256_loadu_pd(src + i), v1 = _mm256_loadu_pd(src + i + 4);
     const __m256d in0 = _mm256_and_pd(_mm256_cmp_pd(v0, lo, _CMP_GE_OQ), _mm256_cmp_pd(v0, hi, _CMP_LE_OQ));
@@ -81,7 +89,7 @@ __attribute__((target("avx2"))) bool narrow_f32_avx2(const double* __restrict__ 
   const __m256d absmask = _mm256_castsi256_pd(_mm256_set1_epi64x(0x7fffffffffffffffLL));
   __m256d ok = _mm256_castsi256_pd(_mm256_set1_epi64x(-1));
   size_t i = 0;
-  const bool nt = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  const bool nt = use_nt() && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
   for (; i + 8 <= cnt; i += 8) {
     const __m256d v0 = _mm256_loadu_pd(src + i), v1 = _mm256_loadu_pd(src + i + 4);
     const __m256d in0 = _mm256_cmp_pd(_mm256_and_pd(v0, absmask), mx, _CMP_LE_OQ);

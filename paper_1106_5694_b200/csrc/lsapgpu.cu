@@ -9,7 +9,10 @@
 // drain the delta log, which it replays in the reference's batch order to
 // reproduce SolveReport::objective_trace and the exact `value == f_start`
 // termination test (parallel.cpp:306-310, 343-345).
+#include <immintrin.h>
+
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
@@ -17,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <string>
@@ -81,7 +85,8 @@ struct Buf {
 };
 
 constexpr size_t kUploadChunk = 64ull << 20;  // rows per H2D chunk: ~64 MB of source
-constexpr int kRing = 3;                       // pinned bounce buffers (pageable sources)
+constexpr size_t kNarrowChunk = 32ull << 20;  // ... for the host-narrowed upload (no per-chunk barrier)
+constexpr int kRing = 4;                       // pinned bounce buffers (pageable sources)
 constexpr size_t kStageKeep = 16ull << 30;     // keep the device staging copy up to this size
 
 int upload_threads() {
@@ -196,6 +201,8 @@ struct lsapgpu_ctx {
   double* obj_pin = nullptr;     // per-job entries of the ordered objective
   int32_t obj_cap = 0;
   LogEntry* log_pin = nullptr;   // delta-log prefix drained with the control block
+  std::vector<LogEntry> log_host, log_sorted;  // replay buffers, kept so their pages stay mapped
+  int64_t host_log_orders = 0;                 // passes whose log the host had to order (device premise failed)
   static constexpr int64_t kLogPin = 1 << 16;
   int64_t log_hint[4] = {kLogPin, kLogPin, kLogPin, kLogPin};  // log entries per outer pass, last solve
 
@@ -335,6 +342,7 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.aux, N, true));
   d.log_cap = std::max<int64_t>(1 << 20, 8 * static_cast<int64_t>(n));
   CK(valloc(ctx, &d.log, static_cast<size_t>(d.log_cap), false));
+  CK(valloc(ctx, &d.log_sorted, static_cast<size_t>(d.log_cap), false));
   d.part_cap = (static_cast<int64_t>(n) + 8) * 16;
   CK(valloc(ctx, &d.part_ad, static_cast<size_t>(d.part_cap), false));
   CK(valloc(ctx, &d.part_at, static_cast<size_t>(d.part_cap), false));
@@ -608,6 +616,13 @@ constexpr int kNarrowFallback = 1000;  // upload_narrow: a value needs a wider t
 // not fit returns kNarrowFallback and the caller redoes the fp64 upload.
 template <class T>
 int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, int32_t ndtype, float probe_amax) {
+  static const bool host_timing = std::getenv("LSAPGPU_HOST_TIMING") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  std::vector<std::pair<const char*, double>> marks;
+  auto mark = [&](const char* what) {
+    if (host_timing)
+      marks.emplace_back(what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count());
+  };
   const size_t row_bytes = static_cast<size_t>(n) * sizeof(T);
   const size_t total = row_bytes * static_cast<size_t>(n);
   if (ctx->stage.bytes < total) {
@@ -617,8 +632,11 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     CK(cudaMalloc(&ctx->stage.p, total));
     ctx->stage.bytes = total;
   }
-  // chunks of ~64 MB of SOURCE (fp64) rows, as the fp64 path
-  int64_t chunk_rows = static_cast<int64_t>(kUploadChunk / (static_cast<size_t>(n) * 8)) / 32 * 32;
+  // chunks of ~32 MB of SOURCE (fp64) rows
+  static const size_t chunk_src = std::getenv("LSAPGPU_NARROW_CHUNK_MB")
+                                      ? static_cast<size_t>(std::max(1, std::atoi(std::getenv("LSAPGPU_NARROW_CHUNK_MB")))) << 20
+                                      : kNarrowChunk;
+  int64_t chunk_rows = static_cast<int64_t>(chunk_src / (static_cast<size_t>(n) * 8)) / 32 * 32;
   if (chunk_rows < 32) chunk_rows = 32;
   if (chunk_rows > n) chunk_rows = n;
   const int nchunks = static_cast<int>((n + chunk_rows - 1) / chunk_rows);
@@ -657,37 +675,83 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   src.src = ctx->stage.p;
   src.src_dtype = ndtype;
   set_source_rows(ctx, &src);
+  // No barrier per chunk: every pool thread walks all chunks, converting its
+  // slice of each into the chunk's pinned ring slot; the calling thread
+  // (t = 0) enqueues chunk k's copy and layout pass as soon as every slice
+  // of it is in.  A thread refills a ring slot only once the copy that last
+  // read it has been enqueued and has completed, so the threads run up to
+  // kRing chunks ahead of the DMA instead of meeting at a join per chunk.
+  mark("setup");
   const int T_ = ctx->pool->size();
-  std::vector<uint8_t> okv(static_cast<size_t>(T_));
-  for (int k = 0; k < nchunks; ++k) {
-    const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
-    const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
-    const size_t cnt = static_cast<size_t>(rows) * static_cast<size_t>(n);
-    const int b = k % kRing;
-    if (k >= kRing) CK(cudaEventSynchronize(ctx->ev_chunk[b]));  // ring slot's previous DMA done
-    T* pin = static_cast<T*>(ctx->ring[b]);
-    const double* hsrc = data + static_cast<size_t>(r0) * static_cast<size_t>(n);
-    ctx->pool->run([&](int t) {  // slices of whole 16-byte groups: streaming stores need the alignment
-      const size_t a = cnt * t / T_ / 8 * 8, e = t + 1 == T_ ? cnt : cnt * (t + 1) / T_ / 8 * 8;
-      okv[t] = narrow_block(hsrc + a, pin + a, e - a) ? 1 : 0;
-    });
-    for (int t = 0; t < T_; ++t)
-      if (!okv[t]) {
-        CK(cudaStreamSynchronize(ctx->copy_stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        return kNarrowFallback;
+  std::unique_ptr<std::atomic<int>[]> filled(new std::atomic<int>[nchunks]);
+  for (int k = 0; k < nchunks; ++k) filled[k].store(0, std::memory_order_relaxed);
+  std::atomic<int> issued{0};   // chunks whose copy (and ring event) is enqueued
+  std::atomic<int> stop{0};     // 1: a value needs a wider type, 2: CUDA error
+  cudaError_t issue_err = cudaSuccess, wait_err = cudaSuccess;
+  const int device = ctx->device;
+  ctx->pool->run([&](int t) {
+    if (t) cudaSetDevice(device);  // the ring events are waited on from every thread
+    for (int k = 0; k < nchunks && !stop.load(std::memory_order_relaxed); ++k) {
+      const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
+      const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
+      const size_t cnt = static_cast<size_t>(rows) * static_cast<size_t>(n);
+      const int b = k % kRing;
+      if (k >= kRing) {  // slot b last held chunk k - kRing
+        while (issued.load(std::memory_order_acquire) <= k - kRing && !stop.load(std::memory_order_relaxed))
+          _mm_pause();
+        if (stop.load(std::memory_order_relaxed)) break;
+        const cudaError_t e = cudaEventSynchronize(ctx->ev_chunk[b]);
+        if (e != cudaSuccess) {
+          wait_err = e;
+          stop.store(2);
+          break;
+        }
       }
-    unsigned char* dst = static_cast<unsigned char*>(ctx->stage.p) + static_cast<size_t>(r0) * row_bytes;
-    CK(cpy(ctx, dst, pin, cnt * sizeof(T), cudaMemcpyHostToDevice, ctx->copy_stream));
-    CK(cudaEventRecord(ctx->ev_chunk[b], ctx->copy_stream));
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_chunk[b], 0));
-    CK(launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
-                           ctx->d.ld, ctx->chunk_flags + k, ctx->stream, qt.bits ? ctx->flags_dev + 2 : nullptr, qt));
-    ++ctx->launches;
+      T* pin = static_cast<T*>(ctx->ring[b]);
+      const double* hsrc = data + static_cast<size_t>(r0) * static_cast<size_t>(n);
+      // slices of whole 16-byte groups: streaming stores need the alignment
+      const size_t a = cnt * t / T_ / 8 * 8, e = t + 1 == T_ ? cnt : cnt * (t + 1) / T_ / 8 * 8;
+      if (!narrow_block(hsrc + a, pin + a, e - a)) {
+        int z = 0;
+        stop.compare_exchange_strong(z, 1);
+        break;
+      }
+      filled[k].fetch_add(1, std::memory_order_release);
+      if (t != 0) continue;
+      while (filled[k].load(std::memory_order_acquire) < T_ && !stop.load(std::memory_order_relaxed)) _mm_pause();
+      if (stop.load(std::memory_order_relaxed)) break;
+      unsigned char* dst = static_cast<unsigned char*>(ctx->stage.p) + static_cast<size_t>(r0) * row_bytes;
+      cudaError_t ce = cpy(ctx, dst, pin, cnt * sizeof(T), cudaMemcpyHostToDevice, ctx->copy_stream);
+      if (ce == cudaSuccess) ce = cudaEventRecord(ctx->ev_chunk[b], ctx->copy_stream);
+      if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ctx->stream, ctx->ev_chunk[b], 0);
+      if (ce == cudaSuccess)
+        ce = launch_layout_fused(src, n, r0, rows, storage, const_cast<void*>(ctx->d.A), const_cast<void*>(ctx->d.AT),
+                                 ctx->d.ld, ctx->chunk_flags + k, ctx->stream,
+                                 qt.bits ? ctx->flags_dev + 2 : nullptr, qt);
+      if (ce != cudaSuccess) {
+        issue_err = ce;
+        stop.store(2);
+        break;
+      }
+      ++ctx->launches;
+      issued.store(k + 1, std::memory_order_release);
+      if (k == 0 || k + 1 == nchunks) mark(k ? "last chunk issued" : "chunk 0 issued");
+    }
+  });
+  if (stop.load() == 2) {
+    CK(issue_err);
+    CK(wait_err);
   }
+  if (stop.load() == 1) {
+    CK(cudaStreamSynchronize(ctx->copy_stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return kNarrowFallback;
+  }
+  mark("host done");
   std::vector<uint32_t> fl(nchunks);
   CK(cpy(ctx, fl.data(), ctx->chunk_flags, sizeof(uint32_t) * nchunks, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  mark("device done");
   uint32_t all = 0;
   for (uint32_t f : fl) all |= f;
   const int final_storage = storage_of_flags(all);
@@ -706,7 +770,15 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
     ctx->stage.p = nullptr;
     ctx->stage.bytes = 0;
   }
-  return finish_matrix(ctx, n);
+  const int frc = finish_matrix(ctx, n);
+  mark("finished");
+  if (host_timing) {
+    std::string line = "lsapgpu upload timing (us, " + std::to_string(nchunks) + " chunks, " +
+                       std::to_string(T_) + " threads):";
+    for (const auto& m : marks) line += std::string(" ") + m.first + "=" + std::to_string(static_cast<int>(m.second));
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
+  return frc;
 }
 
 int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
@@ -1018,17 +1090,16 @@ int run_scan(lsapgpu_ctx* ctx, int full) {
 }
 
 // Stable two-pass counting sort of the delta log by (iter, slot): O(entries + slots).
-void order_log(const std::vector<LogEntry>& in, std::vector<LogEntry>& out, int32_t slots) {
-  const size_t N = in.size();
+void order_log(const LogEntry* in, size_t N, std::vector<LogEntry>& out, int32_t slots) {
   out.resize(N);
   if (N == 0) return;
   static thread_local std::vector<LogEntry> tmp;
   static thread_local std::vector<int64_t> count;
   tmp.resize(N);
   count.assign(static_cast<size_t>(slots) + 1, 0);
-  for (const auto& e : in) ++count[static_cast<size_t>(e.slot) + 1];
+  for (size_t k = 0; k < N; ++k) ++count[static_cast<size_t>(in[k].slot) + 1];
   for (size_t k = 1; k < count.size(); ++k) count[k] += count[k - 1];
-  for (const auto& e : in) tmp[static_cast<size_t>(count[e.slot]++)] = e;
+  for (size_t k = 0; k < N; ++k) tmp[static_cast<size_t>(count[in[k].slot]++)] = in[k];
   int32_t lo = tmp[0].iter, hi = tmp[0].iter;
   for (const auto& e : tmp) {
     lo = std::min(lo, e.iter);
@@ -1643,6 +1714,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   if (!ctx->ctrl_base) CK(cudaMallocHost(&ctx->ctrl_base, sizeof(Ctrl)));
   CK(cpy(ctx, ctx->ctrl_base, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
   double value = 0.0;
+  const int64_t host_orders0 = ctx->host_log_orders;
   Ctrl base;
   std::memset(&base, 0, sizeof(base));
   bool inited = false;
@@ -1698,7 +1770,12 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   ctx->scan_ms = ctx->full_ms = ctx->commit_ms = 0.0;
   ctx->scan_launches = ctx->full_launches = ctx->commit_launches = 0;
   if (!ctx->log_pin) CK(cudaMallocHost(&ctx->log_pin, sizeof(LogEntry) * lsapgpu_ctx::kLogPin));
-  std::vector<LogEntry> log, sorted;
+  // Replay order: see the log read-back below
+  const bool need_order = (trace_switch && trace_value) || d.storage == kF32 || d.storage == kF64;
+  static const bool host_order_env = std::getenv("LSAPGPU_HOST_LOG_ORDER") && std::atoi(std::getenv("LSAPGPU_HOST_LOG_ORDER"));
+  const bool dev_order = need_order && !host_order_env && order_log_fits(n) && d.log_sorted != nullptr;
+  std::vector<LogEntry>& log = ctx->log_host;
+  std::vector<LogEntry>& sorted = ctx->log_sorted;
   int64_t switches = 0;
   int64_t launches = 0;
   int64_t graph_launches = 0;
@@ -1723,6 +1800,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
     S.agent_scans += n;
     S.job_scans += n;
     for (;;) {  // inner loop; repeats only to drain a full delta log
+      bool graph_pass = false;
       if (multi && !dist_graph) {
         for (;;) {
           CK(launch_commit(d, ctx->commit_plan, kCommitSolve, 0, 0, ctx->stream));
@@ -1738,6 +1816,11 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
       } else if (P.use_graph) {
         CK(cudaGraphLaunch(dist_graph ? ctx->dist_exec : ctx->exec, ctx->stream));
         ++graph_launches;
+        graph_pass = true;
+        if (dev_order) {  // the pass's log in batch order, before the read-back below
+          CK(launch_order_log(d, ctx->stream));
+          ++ctx->launches;
+        }
         // control block and the first kLogPin log entries with one sync
         CK(cpy(ctx, ctx->ctrl_host, ctx->ctrl_dev, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
         // log prefix sized from what this pass produced in the previous solve
@@ -1745,7 +1828,8 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         const int hp = std::min<int>(static_cast<int>(S.outer_iterations) - 1, 3);
         pin_len = std::min<int64_t>(std::min<int64_t>(lsapgpu_ctx::kLogPin, d.log_cap),
                                     ctx->log_hint[hp] + ctx->log_hint[hp] / 4 + 1024);
-        CK(cpy(ctx, ctx->log_pin, d.log, sizeof(LogEntry) * pin_len, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cpy(ctx, ctx->log_pin, dev_order ? d.log_sorted : d.log, sizeof(LogEntry) * pin_len,
+               cudaMemcpyDeviceToHost, ctx->stream));
         hmark("graph launched");
         CK(cudaStreamSynchronize(ctx->stream));
         hmark("graph done");
@@ -1772,6 +1856,11 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
           if (C.inner_done || C.expired || C.drain || C.error) break;
         }
       }
+      if (dev_order && !graph_pass) {  // host-stepped passes: order the log now
+        CK(launch_order_log(d, ctx->stream));
+        ++ctx->launches;
+        if ((rc = pull_ctrl(ctx))) return rc;
+      }
       if ((rc = ensure_init())) return rc;
       if (first_pass) f_start = value;
       Ctrl& C = *ctx->ctrl_host;
@@ -1786,30 +1875,52 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
         return fail(ctx, LSAPGPU_ERR_INTERNAL, "internal: conflict check admitted overlapping exchanges");
       }
       const int64_t cnt = C.log_count;
-      const int64_t have = prefetched ? std::min<int64_t>(cnt, pin_len) : 0;
       if (!C.drain) ctx->log_hint[std::min<int>(static_cast<int>(S.outer_iterations) - 1, 3)] = cnt;
       // Replay in the reference's batch order (iteration, then ascending slot:
-      // agents then jobs, parallel.cpp:306-310).  Integer deltas sum exactly in
-      // any order, so without a trace the order only matters for float storage.
-      const bool need_order = (trace_switch && trace_value) || d.storage == kF32 || d.storage == kF64;
+      // agents then jobs, parallel.cpp:306-310), normally ordered on the device
+      // (log_order.cu); the host orders the raw log only if the device could
+      // not.  Integer deltas sum exactly in any order, so without a trace the
+      // order only matters for float storage.
+      const bool sorted_ok = dev_order && C.order_bad == 0 && static_cast<int64_t>(C.order_total) == cnt;
+      const LogEntry* src_dev = sorted_ok ? d.log_sorted : d.log;
+      // (the pinned prefix holds the device-ordered log whenever dev_order)
+      const int64_t have = prefetched && (sorted_ok || !dev_order) ? std::min<int64_t>(cnt, pin_len) : 0;
       const LogEntry* entries = ctx->log_pin;
-      if (need_order || cnt > have) {
+      if (cnt > have) {
         log.resize(static_cast<size_t>(cnt));
         if (have) std::memcpy(log.data(), ctx->log_pin, sizeof(LogEntry) * have);
-        if (cnt > have) {
-          CK(cpy(ctx, log.data() + have, d.log + have, sizeof(LogEntry) * (cnt - have), cudaMemcpyDeviceToHost,
-                 ctx->stream));
-          CK(cudaStreamSynchronize(ctx->stream));
-        }
+        CK(cpy(ctx, log.data() + have, src_dev + have, sizeof(LogEntry) * (cnt - have), cudaMemcpyDeviceToHost,
+               ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
         entries = log.data();
       }
       prefetched = false;
+      hmark("log read");
       if (need_order) {
-        order_log(log, sorted, 2 * n);
-        for (const auto& L : sorted) {
-          value += L.delta;
-          ++switches;
-          trace.push(switches, value);
+        if (!sorted_ok) {
+          order_log(entries, static_cast<size_t>(cnt), sorted, 2 * n);
+          entries = sorted.data();
+          ++ctx->host_log_orders;
+        }
+        hmark("log ordered");
+        if ((d.storage == kI16 || d.storage == kI32) && n < (1 << 22)) {
+          // integer storage: every delta and partial sum is an integer below
+          // 2^53 (n * 2^30 at most), so an int64 running sum converts to the
+          // very doubles the sequential fp64 sum produces, without the fp64
+          // add's latency on the critical path
+          int64_t iv = static_cast<int64_t>(value);
+          for (int64_t k = 0; k < cnt; ++k) {
+            iv += static_cast<int64_t>(entries[k].delta);
+            ++switches;
+            trace.push(switches, static_cast<double>(iv));
+          }
+          value = static_cast<double>(iv);
+        } else {
+          for (int64_t k = 0; k < cnt; ++k) {
+            value += entries[k].delta;
+            ++switches;
+            trace.push(switches, value);
+          }
         }
       } else {
         // integer storage, no trace: every delta and partial sum is an exact
@@ -1873,6 +1984,7 @@ int lsapgpu_solve_dist(lsapgpu_ctx* ctx, const lsapgpu_params* params, const lsa
   S.scan_filter = ctx->scan_plan.filter;
   S.filter_kept = C.filter_kept - base.filter_kept;
   S.filter_overflows = C.filter_overflows - base.filter_overflows;
+  S.host_log_orders = ctx->host_log_orders - host_orders0;
   if (C.fchk_mismatch) {  // LSAPGPU_FILTER_CHECK diagnostics
     char msg[256];
     std::snprintf(msg, sizeof msg,

@@ -65,7 +65,8 @@ struct DevState {
   int32_t* conf_stamp = nullptr;           // agent queued as conflicted in iteration k
   int32_t* rej_stamp = nullptr;            // record slot rejected in iteration k (2n)
   uint32_t* items = nullptr;               // work list (capacity n)
-  LogEntry* log = nullptr;                 // committed exchanges, ordered by (iter, slot) on the host
+  LogEntry* log = nullptr;                 // committed exchanges, in commit order
+  LogEntry* log_sorted = nullptr;          // ... ordered by (iter, slot) on the device (log_order.cu)
   int64_t log_cap = 0;
 
   // split-item partial results (segmented scans)
@@ -215,6 +216,11 @@ cudaError_t launch_commit_cluster(const DevState& d, const CommitPlan& p, int mo
 // step-API helpers
 cudaError_t launch_edges_from_tables(const DevState& d, cudaStream_t st);
 cudaError_t launch_tau16_sync(const DevState& d, cudaStream_t st);
+// Order the delta log by (iter, slot) into log_sorted (the reference's batch
+// order, parallel.cpp:306-310); status in Ctrl::order_bad / order_total.
+// False from order_log_fits when the slot bitmap does not fit shared memory.
+bool order_log_fits(int32_t n);
+cudaError_t launch_order_log(const DevState& d, cudaStream_t st);
 cudaError_t launch_accepted_from_masks(const DevState& d, const uint8_t* agent_acc,
                                        const uint8_t* job_acc, cudaStream_t st);
 

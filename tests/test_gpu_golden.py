@@ -42,6 +42,8 @@ def check(rep, rec):
     assert rep.terminated_by == rec["terminated_by"]
     assert len(rep.objective_trace) == rec["trace_len"]
     assert trace_sha(rep.objective_trace) == rec["trace_sha"]
+    # the delta log was put in batch order on the device (log_order.cu)
+    assert getattr(rep, "gpu", {}).get("host_log_orders", 0) == 0
 
 
 @pytest.mark.parametrize("name", sorted(GOLD["solves"]))
@@ -108,3 +110,38 @@ def test_config_solves_without_trace(gpu_ctx, name, graph):
     assert rep.outer_iterations == rec["outer"]
     assert rep.switches_applied == rec["switches"]
     assert rep.gpu["trace_len"] == rec["trace_len"]
+
+
+ORDER_CASE = r'''
+import sys, json, hashlib; sys.path.insert(0, %r)
+import paper_1106_5694_b200 as g
+ctx = g.Context(0)
+out = {}
+for kind, n, param in (("p2p", 3000, None), ("f32", 2500, None), ("geom", 2000, 100.0)):
+    ctx.generate(kind, n, 1, param)
+    for graph in (True, False):
+        r = ctx.solve(g.ParallelConfig(seed=3, use_graph=graph))
+        out["%%s-%%d-%%d" %% (kind, n, graph)] = [float(r.assignment.value).hex(), r.switches_applied,
+            hashlib.sha256(repr(list(r.objective_trace)).encode()).hexdigest(), r.gpu["host_log_orders"]]
+print(json.dumps(out))
+'''
+
+
+def test_device_log_order_equals_host_order():
+    """The device-ordered delta log (log_order.cu) replays to the same trace
+    and objective bits as the host's own ordering of the raw log
+    (LSAPGPU_HOST_LOG_ORDER=1), for integer, fp32 and fp64 storage, graph
+    and host-stepped passes."""
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(env):
+        r = subprocess.run([sys.executable, "-c", ORDER_CASE % root], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+
+    dev, host = run({}), run({"LSAPGPU_HOST_LOG_ORDER": "1"})
+    assert all(v[3] == 0 for v in dev.values()), dev
+    assert all(v[3] > 0 for v in host.values()), host
+    assert {k: v[:3] for k, v in dev.items()} == {k: v[:3] for k, v in host.items()}
