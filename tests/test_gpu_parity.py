@@ -479,3 +479,19 @@ def test_dgs_beyond_18bit_slots(gpu_ctx):
     assert np.array_equal(np.sort(sig), np.arange(n, dtype=np.int32))
     assert np.array_equal(sig, r2.assignment.sigma) and r1.assignment.value == r2.assignment.value
     assert r1.switches_applied > 0 and r1.outer_iterations >= 2
+
+
+def test_trace_buffers_not_shared_between_live_reports(gpu_ctx):
+    """Context.solve reuses its trace output arrays only once no report views
+    them: a kept report's trace survives later solves unchanged."""
+    import paper_1106_5694_b200 as g
+    gpu_ctx.generate("p2p", 2000, 0)
+    r1 = gpu_ctx.solve(g.ParallelConfig(seed=1))
+    t1 = list(r1.objective_trace)
+    r2 = gpu_ctx.solve(g.ParallelConfig(seed=2))
+    assert list(r2.objective_trace) != t1
+    assert list(r1.objective_trace) == t1
+    del r2
+    r3 = gpu_ctx.solve(g.ParallelConfig(seed=3))  # may reuse r2's arrays
+    assert list(r1.objective_trace) == t1
+    assert list(r3.objective_trace)[0][0] == 0

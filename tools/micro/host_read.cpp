@@ -15,6 +15,9 @@
 #include <thread>
 #include <vector>
 
+// the library's own exact narrowing (host_narrow.cpp), timed in place
+#include "../../paper_1106_5694_b200/csrc/host_narrow.cpp"
+
 static double sum_slice(const double* p, size_t cnt) {
   __m256d a0 = _mm256_setzero_pd(), a1 = a0, a2 = a0, a3 = a0;
   size_t i = 0;
@@ -78,8 +81,13 @@ int main(int argc, char** argv) {
       const size_t a0 = cnt * t / T / 8 * 8, a1 = t + 1 == T ? cnt : cnt * (t + 1) / T / 8 * 8;
       narrow_slice(a.data() + a0, q + a0, a1 - a0);
     });
-    std::printf("threads %2d  read %7.2f ms  %6.1f GB/s   read+narrow-write %7.2f ms  %6.1f GB/s(read)\n", T, ms_r,
-                cnt * 8 / ms_r / 1e6, ms_n, cnt * 8 / ms_n / 1e6);
+    std::vector<int> okv(T);
+    const double ms_l = timed(T, [&](int t) {
+      const size_t a0 = cnt * t / T / 8 * 8, a1 = t + 1 == T ? cnt : cnt * (t + 1) / T / 8 * 8;
+      okv[t] = lsapgpu::narrow_to_i16(a.data() + a0, q + a0, a1 - a0);
+    });
+    std::printf("threads %2d  read %7.2f ms  %6.1f GB/s   read+narrow-write %7.2f ms  %6.1f GB/s   library narrow %7.2f ms  %6.1f GB/s (ok %d)\n",
+                T, ms_r, cnt * 8 / ms_r / 1e6, ms_n, cnt * 8 / ms_n / 1e6, ms_l, cnt * 8 / ms_l / 1e6, okv[0]);
   }
   std::free(q);
   return sink == 12345.0;
