@@ -86,7 +86,9 @@ struct Buf {
 
 constexpr size_t kUploadChunk = 64ull << 20;  // rows per H2D chunk: ~64 MB of source
 constexpr size_t kNarrowChunk = 32ull << 20;  // ... for the host-narrowed upload (no per-chunk barrier)
-constexpr int kRing = 4;                       // pinned bounce buffers (pageable sources)
+constexpr int kRing = 4;                       // pinned bounce buffers (pageable fp64 sources)
+constexpr int kRingNarrow = 8;                 // ... of the host-narrowed upload (absorbs thread skew)
+constexpr int kRingMax = 8;
 constexpr size_t kStageKeep = 16ull << 30;     // keep the device staging copy up to this size
 
 int upload_threads() {
@@ -209,12 +211,12 @@ struct lsapgpu_ctx {
   // host upload pipeline (lsapgpu_set_matrix)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_ready = nullptr;
-  cudaEvent_t ev_chunk[kRing] = {};
+  cudaEvent_t ev_chunk[kRingMax] = {};
   Buf stage;                      // device copy of the source matrix
   uint32_t* chunk_flags = nullptr;
   int chunk_flags_cap = 0;
-  void* ring[kRing] = {};         // pinned bounce buffers
-  size_t ring_bytes = 0;
+  void* ring[kRingMax] = {};      // pinned bounce buffers
+  size_t ring_size[kRingMax] = {};
   HostPool* pool = nullptr;
 
   // auction baseline (auction.cu): per-n vectors (in vec_bufs), the epsilon
@@ -608,6 +610,19 @@ inline bool narrow_block(const double* src, float* dst, size_t cnt) { return lsa
 
 constexpr int kNarrowFallback = 1000;  // upload_narrow: a value needs a wider type; redo as fp64
 
+// pinned bounce buffers 0..slots-1 of at least `bytes` each
+int ensure_ring(lsapgpu_ctx* ctx, int slots, size_t bytes) {
+  for (int k = 0; k < slots; ++k) {
+    if (ctx->ring[k] && ctx->ring_size[k] >= bytes) continue;
+    if (ctx->ring[k]) cudaFreeHost(ctx->ring[k]);
+    ctx->ring[k] = nullptr;
+    ctx->ring_size[k] = 0;
+    CK(cudaMallocHost(&ctx->ring[k], bytes));
+    ctx->ring_size[k] = bytes;
+  }
+  return LSAPGPU_OK;
+}
+
 // The host upload with the matrix narrowed on the HOST (pool threads convert
 // each chunk into the pinned ring as int16 / int32 / fp32, the storage type
 // speculated from the first 64 rows): PCIe then carries 2 or 4 bytes per
@@ -651,14 +666,9 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   CK(cudaMemsetAsync(ctx->flags_dev + 2, 0, sizeof(uint32_t), ctx->stream));  // max |a| (filter scale)
   CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_ready, 0));
-  const size_t ring_bytes = static_cast<size_t>(chunk_rows) * row_bytes;
-  if (ctx->ring_bytes < ring_bytes) {
-    for (auto& r : ctx->ring)
-      if (r) cudaFreeHost(r);
-    for (auto& r : ctx->ring) r = nullptr;
-    ctx->ring_bytes = 0;
-    for (auto& r : ctx->ring) CK(cudaMallocHost(&r, ring_bytes));
-    ctx->ring_bytes = ring_bytes;
+  {
+    const int rc = ensure_ring(ctx, kRingNarrow, static_cast<size_t>(chunk_rows) * row_bytes);
+    if (rc) return rc;
   }
   if (!ctx->pool) ctx->pool = new HostPool(upload_threads());
   {
@@ -680,7 +690,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   // (t = 0) enqueues chunk k's copy and layout pass as soon as every slice
   // of it is in.  A thread refills a ring slot only once the copy that last
   // read it has been enqueued and has completed, so the threads run up to
-  // kRing chunks ahead of the DMA instead of meeting at a join per chunk.
+  // kRingNarrow chunks ahead of the DMA instead of meeting at a join per chunk.
   mark("setup");
   const int T_ = ctx->pool->size();
   std::unique_ptr<std::atomic<int>[]> filled(new std::atomic<int>[nchunks]);
@@ -689,15 +699,20 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   std::atomic<int> stop{0};     // 1: a value needs a wider type, 2: CUDA error
   cudaError_t issue_err = cudaSuccess, wait_err = cudaSuccess;
   const int device = ctx->device;
+  std::vector<double> wait_us(static_cast<size_t>(T_), 0.0), conv_us(static_cast<size_t>(T_), 0.0);
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
   ctx->pool->run([&](int t) {
     if (t) cudaSetDevice(device);  // the ring events are waited on from every thread
     for (int k = 0; k < nchunks && !stop.load(std::memory_order_relaxed); ++k) {
       const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
       const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
       const size_t cnt = static_cast<size_t>(rows) * static_cast<size_t>(n);
-      const int b = k % kRing;
-      if (k >= kRing) {  // slot b last held chunk k - kRing
-        while (issued.load(std::memory_order_acquire) <= k - kRing && !stop.load(std::memory_order_relaxed))
+      const int b = k % kRingNarrow;
+      const double tw0 = host_timing ? now_us() : 0.0;
+      if (k >= kRingNarrow) {  // slot b last held chunk k - kRingNarrow
+        while (issued.load(std::memory_order_acquire) <= k - kRingNarrow && !stop.load(std::memory_order_relaxed))
           _mm_pause();
         if (stop.load(std::memory_order_relaxed)) break;
         const cudaError_t e = cudaEventSynchronize(ctx->ev_chunk[b]);
@@ -711,7 +726,14 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
       const double* hsrc = data + static_cast<size_t>(r0) * static_cast<size_t>(n);
       // slices of whole 16-byte groups: streaming stores need the alignment
       const size_t a = cnt * t / T_ / 8 * 8, e = t + 1 == T_ ? cnt : cnt * (t + 1) / T_ / 8 * 8;
-      if (!narrow_block(hsrc + a, pin + a, e - a)) {
+      const double tw1 = host_timing ? now_us() : 0.0;
+      const bool ok_slice = narrow_block(hsrc + a, pin + a, e - a);
+      if (host_timing) {
+        const double tw2 = now_us();
+        wait_us[t] += tw1 - tw0;
+        conv_us[t] += tw2 - tw1;
+      }
+      if (!ok_slice) {
         int z = 0;
         stop.compare_exchange_strong(z, 1);
         break;
@@ -774,7 +796,9 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   mark("finished");
   if (host_timing) {
     std::string line = "lsapgpu upload timing (us, " + std::to_string(nchunks) + " chunks, " +
-                       std::to_string(T_) + " threads):";
+                       std::to_string(T_) + " threads; thread 1 ring wait " +
+                       std::to_string(static_cast<int>(wait_us[T_ > 1 ? 1 : 0])) + " convert " +
+                       std::to_string(static_cast<int>(conv_us[T_ > 1 ? 1 : 0])) + "):";
     for (const auto& m : marks) line += std::string(" ") + m.first + "=" + std::to_string(static_cast<int>(m.second));
     std::fprintf(stderr, "%s\n", line.c_str());
   }
@@ -851,14 +875,9 @@ int upload_host(lsapgpu_ctx* ctx, const void* data, int32_t n, int32_t dtype) {
                       (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeDevice ||
                        attr.type == cudaMemoryTypeManaged);
   cudaGetLastError();
-  const size_t ring_bytes = static_cast<size_t>(chunk_rows) * row_bytes;
-  if (!pinned && ctx->ring_bytes < ring_bytes) {
-    for (auto& r : ctx->ring)
-      if (r) cudaFreeHost(r);
-    for (auto& r : ctx->ring) r = nullptr;
-    ctx->ring_bytes = 0;
-    for (auto& r : ctx->ring) CK(cudaMallocHost(&r, ring_bytes));
-    ctx->ring_bytes = ring_bytes;
+  if (!pinned) {
+    const int rc = ensure_ring(ctx, kRing, static_cast<size_t>(chunk_rows) * row_bytes);
+    if (rc) return rc;
   }
   if (!pinned && !ctx->pool) ctx->pool = new HostPool(upload_threads());
 
