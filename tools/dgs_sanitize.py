@@ -15,7 +15,7 @@ ctx = g.Context(0)
 for kind, n, param in [("int", 700, 1000.0), ("p2p", 900, None), ("geom", 300, 100.0), ("f32", 500, None)]:
     ctx.generate(kind, n, 1, param)
     for use_graph in graph_modes:
-        for init in ("random", "greedy"):
+        for init in os.environ.get("SANITIZE_INITS", "random,greedy").split(","):
             for pol in ("touched_and_conflicted", "touched_only"):
                 r = ctx.solve(g.ParallelConfig(seed=2, use_graph=use_graph, init=init, reeval=pol))
                 print(kind, n, "graph" if use_graph else "stepped", init, pol, r.assignment.value,
