@@ -575,6 +575,8 @@ cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cuda
 // faster at C4 / C5: the kernel is not short of warps)
 template <class E, class Q, int RB>
 cudaError_t launch_filter_g(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
+  if constexpr (sizeof(Q) == 1)  // 16 int8 positions per lane: one 16-byte chunk load, half the per-chunk overhead
+    if (p.chunk == 16 * 32 * 16) return launch_filter_t<E, Q, RB, 16, 16>(d, p, full, st);
   return launch_filter_t<E, Q, RB, 16, 8>(d, p, full, st);
 }
 

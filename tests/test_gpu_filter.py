@@ -78,6 +78,7 @@ print("ok")
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8"},                       # int8 copies
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "16", "LSAPGPU_FILTER_RB": "1"},  # single row buffer
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_RB": "1"},
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_V": "16"},  # 16 positions per lane
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "0"},                      # every item: exact fallback
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "3"},                      # frequent overflow
 ])
@@ -139,10 +140,11 @@ def _large(n, env):
 
 
 @pytest.mark.parametrize("n,env", [
-    (100000, {}),                                                      # C5 plan: int8 copies, 2 row buffers, 3 slots
-    (100000, {"LSAPGPU_FILTER_RB": "1"}),
+    (100000, {}),                                                      # C5 plan: int8 copies, 1 row buffer, 8 slots
+    (100000, {"LSAPGPU_FILTER_QUEUE": "512"}),
     (60000, {"LSAPGPU_FILTER_BITS": "8"}),
     (100000, {"LSAPGPU_FILTER_CHECK": "7"}),                           # every 7th item re-verified unfiltered
+    (100000, {"LSAPGPU_FILTER_V": "16"}),
 ])
 def test_filter_large_n_deterministic_and_exact(n, env):
     """Repeated solves at C5 size (graph and host-stepped) equal the
