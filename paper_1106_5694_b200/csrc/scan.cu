@@ -170,10 +170,7 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     int want_q = -1;
     if (const char* qq = std::getenv("LSAPGPU_FILTER_QUEUE")) want_q = std::max(0, std::min(kFilterQueueMax, std::atoi(qq)));
     const int threads = 32 * 19;  // 16 consumer warps x 8 positions per lane + 3 role warps
-    // int8 copies: 16 positions per lane (8192-position chunks) when
-    // LSAPGPU_FILTER_V=16; int16 copies always 8 (4096)
-    int want_v = 8;
-    if (const char* v = std::getenv("LSAPGPU_FILTER_V")) want_v = std::atoi(v) == 16 ? 16 : 8;
+    const int32_t chunk = kFilterChunk;
     // prefer int16 copies, then double-buffered rows with a 1024-entry queue
     // and >= 3 slots, then one row buffer (its refill streams from L2: the
     // next row is prefetched; measured faster at C5 than two rows with a
@@ -181,7 +178,6 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     bool done = false;
     for (int qb : {2, 1}) {
       if (want_bits && want_bits != 8 * qb) continue;
-      const int32_t chunk = (qb == 1 && want_v == 16) ? 2 * kFilterChunk : kFilterChunk;
       for (int qcap : {kFilterQueueMax, kFilterQueueMax / 2}) {
         if (want_q >= 0) qcap = want_q;
         for (int rb : {2, 1}) {

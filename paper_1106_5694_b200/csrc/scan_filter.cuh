@@ -572,11 +572,11 @@ cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cuda
 }
 
 // consumer geometry: 16 warps x 8 positions per lane (24 x 4 measured no
-// faster at C4 / C5: the kernel is not short of warps)
+// faster at C4 / C5: the kernel is not short of warps; 16 x 16 for int8
+// copies measured 28% slower at C5, and three rotating aux register sets
+// instead of the copy per chunk 6-17% slower: a later aux load issue)
 template <class E, class Q, int RB>
 cudaError_t launch_filter_g(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  if constexpr (sizeof(Q) == 1)  // 16 int8 positions per lane: one 16-byte chunk load, half the per-chunk overhead
-    if (p.chunk == 16 * 32 * 16) return launch_filter_t<E, Q, RB, 16, 16>(d, p, full, st);
   return launch_filter_t<E, Q, RB, 16, 8>(d, p, full, st);
 }
 

@@ -78,7 +78,6 @@ print("ok")
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8"},                       # int8 copies
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "16", "LSAPGPU_FILTER_RB": "1"},  # single row buffer
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_RB": "1"},
-    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_V": "16"},  # 16 positions per lane
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "0"},                      # every item: exact fallback
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "3"},                      # frequent overflow
 ])
@@ -144,7 +143,6 @@ def _large(n, env):
     (100000, {"LSAPGPU_FILTER_QUEUE": "512"}),
     (60000, {"LSAPGPU_FILTER_BITS": "8"}),
     (100000, {"LSAPGPU_FILTER_CHECK": "7"}),                           # every 7th item re-verified unfiltered
-    (100000, {"LSAPGPU_FILTER_V": "16"}),
 ])
 def test_filter_large_n_deterministic_and_exact(n, env):
     """Repeated solves at C5 size (graph and host-stepped) equal the
