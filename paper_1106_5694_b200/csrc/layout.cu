@@ -88,10 +88,20 @@ __global__ void gen_aux_kernel(LayoutSource s, int32_t n, double* aux) {
 }
 
 // Storage flags of one entry (bit0 non-finite, bit1 not int16-exact, bit2 not
-// an integer below 2^29, bit3 not fp32-exact), with two conversions for the
-// common integer case: one saturating double->int and back decides
-// integrality and both integer ranges; values that are int16-exact are
-// fp32-exact, so the float round trip runs only for the others.
+// an integer below 2^29, bit3 not fp32-exact) from the entry and its two
+// conversions (iv = the saturating double->int, fv = the nearest float),
+// branch-free: the layout pass reuses the same conversions as the stored
+// narrow value, so a C3 entry costs one F2I and one F2F plus compares.
+__device__ __forceinline__ uint32_t entry_flags_c(double v, int32_t iv, float fv) {
+  const bool integral = static_cast<double>(iv) == v;  // (false for NaN / inf)
+  const uint32_t a = static_cast<uint32_t>(iv < 0 ? -static_cast<int64_t>(iv) : iv);
+  uint32_t f = (integral && a <= 32767u) ? 0u : 2u;
+  f |= (integral && a < 536870912u) ? 0u : 4u;
+  f |= (static_cast<double>(fv) == v) ? 0u : 8u;
+  return isfinite(v) ? f : 15u;
+}
+
+// The same, one conversion pair for the common integer case (classify probe).
 __device__ __forceinline__ uint32_t entry_flags(double v) {
   if (!isfinite(v)) return 1u | 2u | 4u | 8u;
   const int32_t iv = __double2int_rz(v);  // saturates
@@ -142,6 +152,18 @@ __device__ __forceinline__ E narrow(double v) {
     return __double2float_rn(v);
   else
     return v;
+}
+
+// narrow<E> from the conversions entry_flags_c already made (non-finite -> 0)
+template <class E>
+__device__ __forceinline__ E narrow_c(double v, int32_t iv, float fv) {
+  const bool fin = isfinite(v);
+  if constexpr (Traits<E>::kInt)
+    return static_cast<E>(fin ? iv : 0);
+  else if constexpr (sizeof(E) == 4)
+    return fin ? fv : 0.f;
+  else
+    return fin ? v : 0.0;
 }
 
 // 32x32 tiles, 32x8 threads: A tile written row-major, AT tile through smem.
@@ -218,7 +240,10 @@ __device__ __forceinline__ void qstore_pair(const QuantTarget& qt, int64_t k, do
   }
 }
 
-template <class E>
+// kF64: the source is an fp64 matrix in memory with an even n (the bench's
+// and every host upload's fallback case): direct 16-byte loads, and none of
+// the generic source code is compiled into the instantiation.
+template <class E, bool kF64>
 __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0, int64_t rows, E* A, E* AT,
                                                            int64_t ld, uint32_t* flags, uint32_t* amax,
                                                            QuantTarget qt) {
@@ -233,16 +258,17 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
   float vmax = 0.f;  // max |entry| rounded up to fp32 (the filter scan's quantization scale)
   // all eight rows' loads first (8 x 16 B in flight per lane), then classify / store
   double v[8][2];
-  const bool fast = src.s.kind == 0 && src.s.src_dtype == 0 && j + 1 < n && (n & 1) == 0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int64_t i = bi + rg + 8 * q;
     v[q][0] = v[q][1] = 0.0;
     if (i >= rend) continue;
-    if (fast) {  // fp64 memory source, even n: both columns in one aligned 16-byte load
-      const double2 w = __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(src.s.src) + i * n + j));
-      v[q][0] = w.x;
-      v[q][1] = w.y;
+    if constexpr (kF64) {  // (n even: j < n implies j + 1 < n)
+      if (j < n) {
+        const double2 w = __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(src.s.src) + i * n + j));
+        v[q][0] = w.x;
+        v[q][1] = w.y;
+      }
     } else {
       if (j < n) v[q][0] = src(i, j);
       if (j + 1 < n) v[q][1] = src(i, j + 1);
@@ -254,13 +280,15 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
     const int64_t i = bi + r;
     if (i >= rend) break;
     const double v0 = v[q][0], v1 = v[q][1];
-    if (j < n) f |= entry_flags(v0);
-    if (j + 1 < n) f |= entry_flags(v1);
+    const int32_t i0 = __double2int_rz(v0), i1 = __double2int_rz(v1);
+    const float f0 = __double2float_rn(v0), f1 = __double2float_rn(v1);
+    if (j < n) f |= entry_flags_c(v0, i0, f0);
+    if (j + 1 < n) f |= entry_flags_c(v1, i1, f1);
     if (amax) {
       if (j < n && isfinite(v0)) vmax = fmaxf(vmax, __double2float_ru(fabs(v0)));
       if (j + 1 < n && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
     }
-    const E e0 = narrow<E>(isfinite(v0) ? v0 : 0.0), e1 = narrow<E>(isfinite(v1) ? v1 : 0.0);
+    const E e0 = narrow_c<E>(v0, i0, f0), e1 = narrow_c<E>(v1, i1, f1);
     const bool own = src.own(i);  // row-block placement: A / Q rows of this rank only
     const int64_t li = src.local(i);
     if (own && j + 1 < n)
@@ -400,8 +428,12 @@ template <class E>
 struct FusedK {
   static void run(dim3 g, dim3 b, cudaStream_t st, Src s, int64_t r0, int64_t rows, void* A, void* AT,
                   int64_t ld, uint32_t* flags, uint32_t* amax, QuantTarget qt) {
-    layout_fused_kernel<E><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags,
-                                           amax, qt);
+    if (s.s.kind == 0 && s.s.src_dtype == 0 && (s.n & 1) == 0)
+      layout_fused_kernel<E, true><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags,
+                                                    amax, qt);
+    else
+      layout_fused_kernel<E, false><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld,
+                                                     flags, amax, qt);
   }
 };
 template <class E>
