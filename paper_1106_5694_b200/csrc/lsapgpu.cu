@@ -335,7 +335,7 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.c_acur, 2 * N2, false));
   CK(valloc(ctx, &d.c_rank, N2, false));
   CK(valloc(ctx, &d.vstate, N, true));
-  CK(valloc(ctx, &d.keys, N + 64, true));  // (cluster commit's global-key variant: 16 slices of ceil(n / 16))
+  CK(valloc(ctx, &d.keys, N, true));
   CK(valloc(ctx, &d.touched_stamp, N, true));
   CK(valloc(ctx, &d.conf_stamp, N, true));
   CK(valloc(ctx, &d.rej_stamp, N2, true));
