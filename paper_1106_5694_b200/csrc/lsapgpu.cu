@@ -686,25 +686,30 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   src.src_dtype = ndtype;
   set_source_rows(ctx, &src);
   // No barrier per chunk: every pool thread walks all chunks, converting its
-  // slice of each into the chunk's pinned ring slot; the calling thread
-  // (t = 0) enqueues chunk k's copy and layout pass as soon as every slice
-  // of it is in.  A thread refills a ring slot only once the copy that last
-  // read it has been enqueued and has completed, so the threads run up to
-  // kRingNarrow chunks ahead of the DMA instead of meeting at a join per chunk.
+  // slice of each into the chunk's pinned ring slot, and the thread that
+  // completes a chunk (the last slice in) enqueues its copy and layout pass
+  // (chunks may go out in any order: each layout pass waits on its own copy
+  // and writes its own rows / columns).  A thread refills a ring slot only
+  // once the copy that last read it has been enqueued and has completed, so
+  // the threads run up to kRingNarrow chunks ahead of the DMA instead of
+  // meeting at a join per chunk, and no thread waits for the others.
   mark("setup");
   const int T_ = ctx->pool->size();
   std::unique_ptr<std::atomic<int>[]> filled(new std::atomic<int>[nchunks]);
   for (int k = 0; k < nchunks; ++k) filled[k].store(0, std::memory_order_relaxed);
-  std::atomic<int> issued{0};   // chunks whose copy (and ring event) is enqueued
+  std::unique_ptr<std::atomic<int>[]> issued(new std::atomic<int>[nchunks]);  // copy + ring event enqueued
+  for (int k = 0; k < nchunks; ++k) issued[k].store(0, std::memory_order_relaxed);
+  std::mutex issue_mu;  // the enqueue (stream order, context counters) is one thread at a time
   std::atomic<int> stop{0};     // 1: a value needs a wider type, 2: CUDA error
   cudaError_t issue_err = cudaSuccess, wait_err = cudaSuccess;
   const int device = ctx->device;
+  cudaSetDevice(device);
   std::vector<double> wait_us(static_cast<size_t>(T_), 0.0), conv_us(static_cast<size_t>(T_), 0.0);
   auto now_us = [] {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   ctx->pool->run([&](int t) {
-    if (t) cudaSetDevice(device);  // the ring events are waited on from every thread
+    if (t) cudaSetDevice(device);  // ring events are waited on, and chunks enqueued, from every thread
     for (int k = 0; k < nchunks && !stop.load(std::memory_order_relaxed); ++k) {
       const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
       const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
@@ -712,7 +717,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
       const int b = k % kRingNarrow;
       const double tw0 = host_timing ? now_us() : 0.0;
       if (k >= kRingNarrow) {  // slot b last held chunk k - kRingNarrow
-        while (issued.load(std::memory_order_acquire) <= k - kRingNarrow && !stop.load(std::memory_order_relaxed))
+        while (!issued[k - kRingNarrow].load(std::memory_order_acquire) && !stop.load(std::memory_order_relaxed))
           _mm_pause();
         if (stop.load(std::memory_order_relaxed)) break;
         const cudaError_t e = cudaEventSynchronize(ctx->ev_chunk[b]);
@@ -738,9 +743,8 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
         stop.compare_exchange_strong(z, 1);
         break;
       }
-      filled[k].fetch_add(1, std::memory_order_release);
-      if (t != 0) continue;
-      while (filled[k].load(std::memory_order_acquire) < T_ && !stop.load(std::memory_order_relaxed)) _mm_pause();
+      if (filled[k].fetch_add(1, std::memory_order_acq_rel) != T_ - 1) continue;  // not the last slice
+      std::lock_guard<std::mutex> lk(issue_mu);
       if (stop.load(std::memory_order_relaxed)) break;
       unsigned char* dst = static_cast<unsigned char*>(ctx->stage.p) + static_cast<size_t>(r0) * row_bytes;
       cudaError_t ce = cpy(ctx, dst, pin, cnt * sizeof(T), cudaMemcpyHostToDevice, ctx->copy_stream);
@@ -756,7 +760,7 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
         break;
       }
       ++ctx->launches;
-      issued.store(k + 1, std::memory_order_release);
+      issued[k].store(1, std::memory_order_release);
       if (k == 0 || k + 1 == nchunks) mark(k ? "last chunk issued" : "chunk 0 issued");
     }
   });
