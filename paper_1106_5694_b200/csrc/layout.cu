@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
       if (j + 1 < n) v[q][1] = src(i, j + 1);
     }
   }
+  // column guards (kF64: n even, so both columns of a lane are in or out together)
+  const bool jv0 = j < n, jv1 = kF64 ? jv0 : j + 1 < n;
+  const bool all_rows = src.s.a_rows < 0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int r = rg + 8 * q;
@@ -282,23 +285,22 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
     const double v0 = v[q][0], v1 = v[q][1];
     const int32_t i0 = __double2int_rz(v0), i1 = __double2int_rz(v1);
     const float f0 = __double2float_rn(v0), f1 = __double2float_rn(v1);
-    if (j < n) f |= entry_flags_c(v0, i0, f0);
-    if (j + 1 < n) f |= entry_flags_c(v1, i1, f1);
+    f |= (jv0 ? entry_flags_c(v0, i0, f0) : 0u) | (jv1 ? entry_flags_c(v1, i1, f1) : 0u);
     if (amax) {
-      if (j < n && isfinite(v0)) vmax = fmaxf(vmax, __double2float_ru(fabs(v0)));
-      if (j + 1 < n && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
+      if (jv0 && isfinite(v0)) vmax = fmaxf(vmax, __double2float_ru(fabs(v0)));
+      if (jv1 && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
     }
     const E e0 = narrow_c<E>(v0, i0, f0), e1 = narrow_c<E>(v1, i1, f1);
-    const bool own = src.own(i);  // row-block placement: A / Q rows of this rank only
-    const int64_t li = src.local(i);
-    if (own && j + 1 < n)
+    const bool own = all_rows || src.own(i);  // row-block placement: A / Q rows of this rank only
+    const int64_t li = all_rows ? i : src.local(i);
+    if (own && jv1)
       Pair<E>::st(A + li * ld + j, e0, e1);
-    else if (own && j < n)
+    else if (own && jv0)
       A[li * ld + j] = e0;
     tile[r][2 * lane] = e0;
     tile[r][2 * lane + 1] = e1;
-    if (qt.bits && own && j < n)
-      qstore_pair(qt, li * ld + j, static_cast<double>(e0), static_cast<double>(e1), j + 1 < n);
+    if (qt.bits && own && jv0)
+      qstore_pair(qt, li * ld + j, static_cast<double>(e0), static_cast<double>(e1), jv1);
   }
   __syncthreads();
   // AT rows bj .. bj+63, columns (agents) bi .. bi+63
