@@ -10,8 +10,6 @@
 //   100k x 100k instance never exists in host memory or as an fp64 copy.
 #include <cmath>
 
-#include <algorithm>
-
 #include "state.h"
 
 namespace lsapgpu {
@@ -250,80 +248,74 @@ __global__ void __launch_bounds__(256) layout_fused_kernel(Src src, int64_t row0
                                                            int64_t ld, uint32_t* flags, uint32_t* amax,
                                                            QuantTarget qt) {
   __shared__ E tile[64][66];
+  const int64_t bi = row0 + static_cast<int64_t>(blockIdx.y) * 64;  // agent block
+  const int64_t bj = static_cast<int64_t>(blockIdx.x) * 64;         // job block
   const int n = src.n;
   const int64_t rend = row0 + rows;
   const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;  // 8 row groups
+  const int64_t j = bj + 2 * lane;
   uint32_t f = 0;
   float vmax = 0.f;  // max |entry| rounded up to fp32 (the filter scan's quantization scale)
-  // persistent blocks walk the 64 x 64 tiles (block setup and the flag /
-  // max reductions once per block, not per tile)
-  const int64_t tiles_x = (n + 63) / 64, tiles = tiles_x * ((rows + 63) / 64);
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t bi = row0 + (t / tiles_x) * 64;  // agent block
-    const int64_t bj = (t % tiles_x) * 64;         // job block
-    const int64_t j = bj + 2 * lane;
-    // all eight rows' loads first (8 x 16 B in flight per lane), then classify / store
-    double v[8][2];
+  // all eight rows' loads first (8 x 16 B in flight per lane), then classify / store
+  double v[8][2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int64_t i = bi + rg + 8 * q;
-      v[q][0] = v[q][1] = 0.0;
-      if (i >= rend) continue;
-      if constexpr (kF64) {  // (n even: j < n implies j + 1 < n)
-        if (j < n) {
-          const double2 w = __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(src.s.src) + i * n + j));
-          v[q][0] = w.x;
-          v[q][1] = w.y;
-        }
-      } else {
-        if (j < n) v[q][0] = src(i, j);
-        if (j + 1 < n) v[q][1] = src(i, j + 1);
+  for (int q = 0; q < 8; ++q) {
+    const int64_t i = bi + rg + 8 * q;
+    v[q][0] = v[q][1] = 0.0;
+    if (i >= rend) continue;
+    if constexpr (kF64) {  // (n even: j < n implies j + 1 < n)
+      if (j < n) {
+        const double2 w = __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(src.s.src) + i * n + j));
+        v[q][0] = w.x;
+        v[q][1] = w.y;
       }
+    } else {
+      if (j < n) v[q][0] = src(i, j);
+      if (j + 1 < n) v[q][1] = src(i, j + 1);
     }
-    // column guards (kF64: n even, so both columns of a lane are in or out together)
-    const bool jv0 = j < n, jv1 = kF64 ? jv0 : j + 1 < n;
-    const bool all_rows = src.s.a_rows < 0;
+  }
+  // column guards (kF64: n even, so both columns of a lane are in or out together)
+  const bool jv0 = j < n, jv1 = kF64 ? jv0 : j + 1 < n;
+  const bool all_rows = src.s.a_rows < 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int r = rg + 8 * q;
-      const int64_t i = bi + r;
-      if (i >= rend) break;
-      const double v0 = v[q][0], v1 = v[q][1];
-      const int32_t i0 = __double2int_rz(v0), i1 = __double2int_rz(v1);
-      const float f0 = __double2float_rn(v0), f1 = __double2float_rn(v1);
-      f |= (jv0 ? entry_flags_c(v0, i0, f0) : 0u) | (jv1 ? entry_flags_c(v1, i1, f1) : 0u);
-      if (amax) {
-        if (jv0 && isfinite(v0)) vmax = fmaxf(vmax, __double2float_ru(fabs(v0)));
-        if (jv1 && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
-      }
-      const E e0 = narrow_c<E>(v0, i0, f0), e1 = narrow_c<E>(v1, i1, f1);
-      const bool own = all_rows || src.own(i);  // row-block placement: A / Q rows of this rank only
-      const int64_t li = all_rows ? i : src.local(i);
-      if (own && jv1)
-        Pair<E>::st(A + li * ld + j, e0, e1);
-      else if (own && jv0)
-        A[li * ld + j] = e0;
-      tile[r][2 * lane] = e0;
-      tile[r][2 * lane + 1] = e1;
-      if (qt.bits && own && jv0)
-        qstore_pair(qt, li * ld + j, static_cast<double>(e0), static_cast<double>(e1), jv1);
+  for (int q = 0; q < 8; ++q) {
+    const int r = rg + 8 * q;
+    const int64_t i = bi + r;
+    if (i >= rend) break;
+    const double v0 = v[q][0], v1 = v[q][1];
+    const int32_t i0 = __double2int_rz(v0), i1 = __double2int_rz(v1);
+    const float f0 = __double2float_rn(v0), f1 = __double2float_rn(v1);
+    f |= (jv0 ? entry_flags_c(v0, i0, f0) : 0u) | (jv1 ? entry_flags_c(v1, i1, f1) : 0u);
+    if (amax) {
+      if (jv0 && isfinite(v0)) vmax = fmaxf(vmax, __double2float_ru(fabs(v0)));
+      if (jv1 && isfinite(v1)) vmax = fmaxf(vmax, __double2float_ru(fabs(v1)));
     }
-    __syncthreads();
-    // AT rows bj .. bj+63, columns (agents) bi .. bi+63
-    const int64_t ia = bi + 2 * lane;
-    for (int c = rg; c < 64; c += 8) {
-      const int64_t jj = bj + c;
-      if (jj >= n) break;
-      E* at = AT + jj * ld + ia;
-      if (ia + 1 < rend)
-        Pair<E>::st(at, tile[2 * lane][c], tile[2 * lane + 1][c]);
-      else if (ia < rend)
-        at[0] = tile[2 * lane][c];
-      if (qt.bits && ia < rend)  // QT = the same values quantized, transposed
-        qstore_pair(QuantTarget{qt.QT, nullptr, qt.scale, qt.bits}, jj * ld + ia, static_cast<double>(tile[2 * lane][c]),
-                    static_cast<double>(tile[2 * lane + 1][c]), ia + 1 < rend);
-    }
-    __syncthreads();  // the next tile reuses the staging tile
+    const E e0 = narrow_c<E>(v0, i0, f0), e1 = narrow_c<E>(v1, i1, f1);
+    const bool own = all_rows || src.own(i);  // row-block placement: A / Q rows of this rank only
+    const int64_t li = all_rows ? i : src.local(i);
+    if (own && jv1)
+      Pair<E>::st(A + li * ld + j, e0, e1);
+    else if (own && jv0)
+      A[li * ld + j] = e0;
+    tile[r][2 * lane] = e0;
+    tile[r][2 * lane + 1] = e1;
+    if (qt.bits && own && jv0)
+      qstore_pair(qt, li * ld + j, static_cast<double>(e0), static_cast<double>(e1), jv1);
+  }
+  __syncthreads();
+  // AT rows bj .. bj+63, columns (agents) bi .. bi+63
+  const int64_t ia = bi + 2 * lane;
+  for (int c = rg; c < 64; c += 8) {
+    const int64_t jj = bj + c;
+    if (jj >= n) break;
+    E* at = AT + jj * ld + ia;
+    if (ia + 1 < rend)
+      Pair<E>::st(at, tile[2 * lane][c], tile[2 * lane + 1][c]);
+    else if (ia < rend)
+      at[0] = tile[2 * lane][c];
+    if (qt.bits && ia < rend)  // QT = the same values quantized, transposed
+      qstore_pair(QuantTarget{qt.QT, nullptr, qt.scale, qt.bits}, jj * ld + ia, static_cast<double>(tile[2 * lane][c]),
+                  static_cast<double>(tile[2 * lane + 1][c]), ia + 1 < rend);
   }
   for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
   __shared__ uint32_t wf[8];
@@ -507,10 +499,7 @@ cudaError_t launch_layout_fused(const LayoutSource& s, int32_t n, int64_t row0, 
                                 void* A, void* AT, int64_t ld, uint32_t* flags, cudaStream_t st, uint32_t* amax,
                                 QuantTarget qt) {
   Src src{s, n};
-  const int64_t tiles = ((static_cast<int64_t>(n) + 63) / 64) * ((rows + 63) / 64);
-  int sms = 148, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const dim3 g(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tiles, 8LL * sms))));
+  dim3 g(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
   return dispatch<FusedK>(storage, g, dim3(256), st, src, row0, rows, A, AT, ld, flags, amax, qt);
 }
 
