@@ -240,6 +240,69 @@ __device__ __forceinline__ void qstore_pair(const QuantTarget& qt, int64_t k, do
   }
 }
 
+// The common case on its own: an fp64 matrix in memory with an even n, every
+// row of A held, no max|a| and no filter copies (C1-C3 from a device matrix
+// or the host fallback).  Same tiles and results as layout_fused_kernel, with
+// no per-element guards beyond the row / column range and incremented
+// pointers, so the pass is no longer instruction-bound.
+template <class E>
+__global__ void __launch_bounds__(256) layout_plain_kernel(const double* __restrict__ src, int32_t n, int64_t row0,
+                                                           int64_t rows, E* __restrict__ A, E* __restrict__ AT,
+                                                           int64_t ld, uint32_t* flags) {
+  __shared__ E tile[64][66];
+  const int64_t bi = row0 + static_cast<int64_t>(blockIdx.y) * 64;  // agent block
+  const int32_t bj = static_cast<int32_t>(blockIdx.x) * 64;         // job block
+  const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;         // 8 row groups
+  const int32_t j = bj + 2 * lane;
+  const bool jv = j < n;  // (n even: both columns of the lane, or neither)
+  const int64_t rend = row0 + rows;
+  const int64_t left = rend - bi - rg;  // rows of this thread in the tile: rg, rg + 8, ...
+  const int nq = left <= 0 ? 0 : (left >= 57 ? 8 : static_cast<int>((left + 7) / 8));
+  double2 v[8];
+  const double* sp = src + (bi + rg) * static_cast<int64_t>(n) + j;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    v[q] = (q < nq && jv) ? __ldg(reinterpret_cast<const double2*>(sp + static_cast<int64_t>(8 * q) * n))
+                          : make_double2(0.0, 0.0);
+  uint32_t f = 0;
+  E* ap = A + (bi + rg) * ld + j;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q >= nq) break;
+    const int32_t i0 = __double2int_rz(v[q].x), i1 = __double2int_rz(v[q].y);
+    const float f0 = __double2float_rn(v[q].x), f1 = __double2float_rn(v[q].y);
+    const E e0 = narrow_c<E>(v[q].x, i0, f0), e1 = narrow_c<E>(v[q].y, i1, f1);
+    if (jv) {
+      f |= entry_flags_c(v[q].x, i0, f0) | entry_flags_c(v[q].y, i1, f1);
+      Pair<E>::st(ap + static_cast<int64_t>(8 * q) * ld, e0, e1);
+    }
+    tile[rg + 8 * q][2 * lane] = e0;
+    tile[rg + 8 * q][2 * lane + 1] = e1;
+  }
+  __syncthreads();
+  // AT rows bj .. bj+63, columns (agents) bi .. bi+63
+  const int64_t ia = bi + 2 * lane;
+  const bool iv1 = ia + 1 < rend, iv0 = ia < rend;
+  E* atp = AT + static_cast<int64_t>(bj + rg) * ld + ia;
+#pragma unroll
+  for (int c = rg; c < 64; c += 8, atp += 8 * ld) {
+    if (bj + c >= n) break;
+    if (iv1)
+      Pair<E>::st(atp, tile[2 * lane][c], tile[2 * lane + 1][c]);
+    else if (iv0)
+      atp[0] = tile[2 * lane][c];
+  }
+  for (int off = 16; off > 0; off >>= 1) f |= __shfl_down_sync(0xffffffffu, f, off);
+  __shared__ uint32_t wf[8];
+  if (lane == 0) wf[rg] = f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (int w = 0; w < 8; ++w) r |= wf[w];
+    if (r) atomicOr(flags, r);
+  }
+}
+
 // kF64: the source is an fp64 matrix in memory with an even n (the bench's
 // and every host upload's fallback case): direct 16-byte loads, and none of
 // the generic source code is compiled into the instantiation.
@@ -430,7 +493,10 @@ template <class E>
 struct FusedK {
   static void run(dim3 g, dim3 b, cudaStream_t st, Src s, int64_t r0, int64_t rows, void* A, void* AT,
                   int64_t ld, uint32_t* flags, uint32_t* amax, QuantTarget qt) {
-    if (s.s.kind == 0 && s.s.src_dtype == 0 && (s.n & 1) == 0)
+    if (s.s.kind == 0 && s.s.src_dtype == 0 && (s.n & 1) == 0 && s.s.a_rows < 0 && !amax && !qt.bits)
+      layout_plain_kernel<E><<<g, b, 0, st>>>(static_cast<const double*>(s.s.src), s.n, r0, rows, static_cast<E*>(A),
+                                              static_cast<E*>(AT), ld, flags);
+    else if (s.s.kind == 0 && s.s.src_dtype == 0 && (s.n & 1) == 0)
       layout_fused_kernel<E, true><<<g, b, 0, st>>>(s, r0, rows, static_cast<E*>(A), static_cast<E*>(AT), ld, flags,
                                                     amax, qt);
     else
