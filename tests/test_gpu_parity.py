@@ -101,6 +101,28 @@ def test_matrix_dtypes_and_device_upload(oracle, gpu_ctx):
         assert tables_equal(gpu_ctx.evaluate_all(sigma), *expect)
 
 
+@pytest.mark.parametrize("n", [2, 64, 66, 130, 1000, 1002])
+def test_device_fp64_layout_tiles_and_storage(oracle, gpu_ctx, n):
+    """The device fp64 layout pass (csrc/layout.cu, the plain kernel for
+    even n) at tile edges: ragged last tiles in both directions, every
+    storage class it can pick, and a non-finite entry anywhere."""
+    import torch
+    rng = np.random.default_rng(n)
+    sigma = oracle.random_perm(n, 3)
+    cases = [("int16", rng.integers(-30000, 30000, (n, n)).astype(np.float64)),
+             ("int32", rng.integers(-2000000, 2000000, (n, n)).astype(np.float64)),
+             ("fp32", np.asarray(rng.random((n, n)), np.float32).astype(np.float64)),
+             ("fp64", rng.random((n, n)))]
+    for storage, a in cases:
+        gpu_ctx.set_matrix(torch.from_numpy(a).cuda())
+        assert gpu_ctx.storage == storage, (n, storage)
+        assert tables_equal(gpu_ctx.evaluate_all(sigma), *oracle.evaluate_all(a, sigma)), (n, storage)
+    bad = cases[0][1].copy()
+    bad[n // 2, n - 1] = np.nan
+    with pytest.raises(Exception, match="non-finite"):
+        gpu_ctx.set_matrix(torch.from_numpy(bad).cuda())
+
+
 def test_generators_match_oracle(oracle, gpu_ctx):
     for kind, n, seed, param in [("int", 70, 3, 1000), ("f32", 70, 4, None), ("unit", 70, 5, 10.0),
                                  ("p2p", 70, 6, None), ("geom", 70, 7, 100.0)]:
