@@ -170,6 +170,18 @@ __global__ void __launch_bounds__(kResThreads, 1)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  // barrier setup reads nothing the previous kernel writes: done before the wait
+  if (tid == 0) {
+    for (int k = 0; k < bufs; ++k) {
+      mbar_init(&full_bar[k], 1);
+      mbar_init(&empty_bar[k], NW);
+      arrive_cnt[k] = 0;
+    }
+    mbar_init(res_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    ebuf_n = 0;
+  }
+  __syncthreads();
   pdl_trigger();  // persistent single-wave grid: the next kernel may queue now
   pdl_wait();     // the commit / apply before this scan wrote the state it reads
   if (blockIdx.x == 0 && tid == 0) tl_mark(st.ctrl, st.tl, st.tl_cap, full ? kTlScanFull : kTlScan);
@@ -198,17 +210,6 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const int parity_out = st.ctrl->parity;
   const int64_t stages = (units - blockIdx.x + gridDim.x - 1) / gridDim.x;  // one per unit
 
-  if (tid == 0) {
-    for (int k = 0; k < bufs; ++k) {
-      mbar_init(&full_bar[k], 1);
-      mbar_init(&empty_bar[k], NW);
-      arrive_cnt[k] = 0;
-    }
-    mbar_init(res_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    ebuf_n = 0;
-  }
-  __syncthreads();
 
   if (warp == NW) {
     // ---------------- producer warp ----------------
