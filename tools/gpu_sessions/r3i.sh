@@ -5,4 +5,4 @@ run f_geom_random_greedyonly_random $S python tools/sanitize_min.py geom 300 ran
 run g_int_random_greedyonly_random $S python tools/sanitize_min.py int 700 random,greedy_only,random 1
 SANITIZE_INITS=random run h_full_random_graph $S python tools/dgs_sanitize.py graph
 SANITIZE_INITS=random LSAPGPU_SCAN_FILTER=2 run i_full_random_graph_filter $S python tools/dgs_sanitize.py graph
-bash tools/r3f.sh
+bash tools/gpu_sessions/r3f.sh
