@@ -1394,9 +1394,9 @@ int32_t lsapgpu_timeline(lsapgpu_ctx* ctx, uint64_t* out, int32_t capacity) {
 int lsapgpu_scan_plan(const lsapgpu_ctx* ctx, int32_t* info, int32_t cap) {
   if (!ctx || !info || cap < 0) return LSAPGPU_ERR_INVALID;
   const ScanPlan& p = ctx->scan_plan;
-  const int32_t v[9] = {p.filter ? 2 : (p.resident ? 1 : 0), p.m, p.bufs, p.filter, p.ctas, p.threads,
-                        static_cast<int32_t>(p.smem), static_cast<int32_t>(p.chunk), p.filter_queue};
-  const int32_t k = cap < 9 ? cap : 9;
+  const int32_t v[10] = {p.filter ? 2 : (p.resident ? 1 : 0), p.m, p.bufs, p.filter, p.ctas, p.threads,
+                         static_cast<int32_t>(p.smem), static_cast<int32_t>(p.chunk), p.filter_queue, p.filter_tmem};
+  const int32_t k = cap < 10 ? cap : 10;
   for (int32_t q = 0; q < k; ++q) info[q] = v[q];
   return k;
 }

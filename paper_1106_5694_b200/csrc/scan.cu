@@ -171,6 +171,10 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
     if (const char* qq = std::getenv("LSAPGPU_FILTER_QUEUE")) want_q = std::max(0, std::min(kFilterQueueMax, std::atoi(qq)));
     const int threads = 32 * 19;  // 16 consumer warps x 8 positions per lane + 3 role warps
     const int32_t chunk = kFilterChunk;
+    // aux[] resident in tensor memory where it fits (n <= 65536; measured at
+    // C4: full sweep 0.85 -> 0.69 ms); LSAPGPU_FILTER_TMEM=0 keeps it in L2
+    int tmem_aux = 1;
+    if (const char* t = std::getenv("LSAPGPU_FILTER_TMEM")) tmem_aux = std::atoi(t) != 0;
     // prefer int16 copies, then double-buffered rows with a 1024-entry queue
     // and >= 3 slots, then one row buffer (its refill streams from L2: the
     // next row is prefetched; measured faster at C5 than two rows with a
@@ -197,6 +201,8 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
           p.max_segments = 1;
           p.l2_prefetch = 0;
           p.filter_queue = qcap;
+          // aux[] in tensor memory: 32 * chunks columns of 512 (n <= 65536)
+          p.filter_tmem = tmem_aux && (d.n + chunk - 1) / chunk <= 16 ? 1 : 0;
           done = true;
           break;
         }

@@ -84,6 +84,34 @@ __device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, uint32_t dep) {
       : "memory");
 }
 
+// Tensor memory (TMEM) holding the launch's aux[] words when they fit (C4):
+// consumer warp w keeps the words of its positions in TMEM lane quarter w % 4,
+// columns (w / 4) * nch * V + c * V .. + V - 1 for chunk c, and reads a
+// chunk's V words with one 32x32b load instead of V / 4 L2 loads per item.
+__device__ __forceinline__ void tmem_alloc512(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst_smem))
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&w)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&w)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ int32_t eps_gate(double sv, double eps, double S) {
   const double r = floor((sv + eps) * S);
   if (!(r < 1e9)) return 1 << 24;  // (also NaN-safe) nothing can be active
@@ -123,9 +151,10 @@ __device__ __forceinline__ uint4 lds_q(const unsigned char* p) {
   }
 }
 
-template <class E, class Q, int RB, int W, int V>
+template <class E, class Q, int RB, int W, int V, bool kTM>
 __global__ void __launch_bounds__(32 * (W + 3), 1)
     pair_scan_filter_kernel(DevState st, int full, int NS, int qcap) {
+  static_assert(!kTM || V == 8, "TMEM aux: 8 words per lane per chunk");
   // the geometry of this instantiation (shadowing the default constants)
   constexpr int kFW = W;
   constexpr int kFV = V;
@@ -193,7 +222,29 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
     ebuf_n = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __shared__ uint32_t tmem_base_s;
+  if constexpr (kTM) {
+    if (warp == 0) tmem_alloc512(&tmem_base_s);  // one CTA per SM: the whole TMEM
+    tmem_fence_before();
+  }
   __syncthreads();
+  uint32_t tmem_base = 0;
+  if constexpr (kTM) {
+    tmem_fence_after();
+    tmem_base = tmem_base_s;
+    if (warp < kFW) {  // each consumer warp stores the aux words of its own positions, every chunk
+      const int32_t lo0 = warp * kFBlk + lane * kFV;
+      const uint32_t tw = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                          static_cast<uint32_t>((warp >> 2) * nch * kFV);
+      for (int32_t c = 0; c < nch; ++c) {
+        const int64_t p = static_cast<int64_t>(c) * kFChunk + lo0;
+        AuxW<kFV> x;
+        ld_aux<kFV>(x, aux_g + p, p < n);
+        tmem_st8(tw + static_cast<uint32_t>(c * kFV), x.w);
+      }
+      tmem_wait_st();
+    }
+  }
 
   auto item_of = [&](int32_t q) -> FInfo {
     FInfo it;
@@ -451,8 +502,12 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
     // chunk's compute (long-scoreboard stalls with a one-chunk lead)
     AuxW<kFV> nx, fx;
     int32_t cnext = nch > 1 ? 1 : 0;  // chunk held in fx
-    load_aux(0, nx);
-    load_aux(cnext, fx);
+    if constexpr (!kTM) {
+      load_aux(0, nx);
+      load_aux(cnext, fx);
+    }
+    const uint32_t tw = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                        static_cast<uint32_t>((warp >> 2) * nch * kFV);
     for (int32_t q = 0; q < stages; ++q) {
       const int rb = q % RB;
       const int par = q & 1;
@@ -463,11 +518,17 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
       int32_t T = t0;
       int32_t tshare = kFNeg;  // last read of tmax[par]
       for (int32_t c = 0; c < nch; ++c) {
-        const AuxW<kFV> ax = nx;
-        nx = fx;
-        cnext = cnext + 1 < nch ? cnext + 1 : 0;  // chunk c + 2 (wrapping into the next item)
-        load_aux(cnext, fx);
+        AuxW<kFV> ax;
+        if constexpr (kTM) {
+          tmem_ld8(tw + static_cast<uint32_t>(c * kFV), ax.w);  // completes behind the slot wait
+        } else {
+          ax = nx;
+          nx = fx;
+          cnext = cnext + 1 < nch ? cnext + 1 : 0;  // chunk c + 2 (wrapping into the next item)
+          load_aux(cnext, fx);
+        }
         mbar_wait_backoff(&slot_full[s], fph, 20);
+        if constexpr (kTM) tmem_wait_ld();
         const unsigned char* sb = slots + s * kSlotBytes;
         const uint4 qv = lds_q<Q, kFV>(sb + lo * static_cast<int>(sizeof(Q)));
         const uint32_t(&aw)[kFV] = ax.w;
@@ -532,7 +593,12 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
       mbar_arrive_after(&item_done[par], static_cast<uint32_t>(tshare));
     }
   }
+  if constexpr (kTM) tmem_fence_before();
   __syncthreads();
+  if constexpr (kTM) {
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc512(tmem_base);
+  }
   const int ne = min(ebuf_n, kFEdgeBuf);
   __shared__ int gbase;
   if (tid == 0 && ne > 0) gbase = atomicAdd(&st.ctrl->edge_count[parity_out], ne);
@@ -561,11 +627,11 @@ __global__ void filter_aux_kernel(DevState st) {
   }
 }
 
-template <class E, class Q, int RB, int W, int V>
+template <class E, class Q, int RB, int W, int V, bool kTM>
 cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
   cudaError_t e = launch_pdl(filter_aux_kernel<E, Q>, dim3(p.ctas), dim3(256), 0, st, d.pdl, d);
   if (e != cudaSuccess) return e;
-  auto k = pair_scan_filter_kernel<E, Q, RB, W, V>;
+  auto k = pair_scan_filter_kernel<E, Q, RB, W, V, kTM>;
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;
   return launch_pdl(k, dim3(p.ctas), dim3(32 * (W + 3)), p.smem, st, d.pdl, d, full, p.bufs, p.filter_queue);
@@ -577,7 +643,8 @@ cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cuda
 // instead of the copy per chunk 6-17% slower: a later aux load issue)
 template <class E, class Q, int RB>
 cudaError_t launch_filter_g(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  return launch_filter_t<E, Q, RB, 16, 8>(d, p, full, st);
+  if (p.filter_tmem) return launch_filter_t<E, Q, RB, 16, 8, true>(d, p, full, st);
+  return launch_filter_t<E, Q, RB, 16, 8, false>(d, p, full, st);
 }
 
 }  // namespace scan_detail

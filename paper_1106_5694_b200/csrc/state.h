@@ -159,12 +159,13 @@ struct ScanPlan {
   int filter = 0;       // 8 / 16: quantized-filter kernel (scan_filter.cuh) with int8 / int16 copies;
                         // m = row buffers, bufs = chunk slots
   int filter_queue = 1024;  // filter kernel: candidates per item before the exact whole-item fallback
+  int filter_tmem = 0;      // filter kernel: the launch's aux words resident in TMEM (n <= 65536)
   int launches() const { return filter ? 2 : 1; }  // kernels per scan (the filter adds the aux build)
   bool operator==(const ScanPlan& o) const {
     return m == o.m && passes == o.passes && chunk == o.chunk && bufs == o.bufs && ctas == o.ctas &&
            threads == o.threads && smem == o.smem && max_segments == o.max_segments && resident == o.resident &&
            depth == o.depth && l2_prefetch == o.l2_prefetch && filter == o.filter &&
-           filter_queue == o.filter_queue;
+           filter_queue == o.filter_queue && filter_tmem == o.filter_tmem;
   }
 };
 ScanPlan plan_scan(const DevState& d, int num_sms);

@@ -626,7 +626,7 @@ class Context:
         k = N.LIB.lsapgpu_scan_plan(self.h, N.ptr(info), 16)
         if k < 0:
             self._check(k)
-        names = ["kernel", "m", "bufs", "filter", "ctas", "threads", "smem", "chunk", "filter_queue"]
+        names = ["kernel", "m", "bufs", "filter", "ctas", "threads", "smem", "chunk", "filter_queue", "filter_tmem"]
         out = dict(zip(names, info[:k].tolist()))
         out["kernel"] = ["streaming", "resident", "filter"][out["kernel"]]
         return out

@@ -78,6 +78,8 @@ print("ok")
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8"},                       # int8 copies
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "16", "LSAPGPU_FILTER_RB": "1"},  # single row buffer
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_RB": "1"},
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_TMEM": "0"},                       # aux[] from L2, not TMEM
+    {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_TMEM": "0", "LSAPGPU_FILTER_BITS": "8", "LSAPGPU_FILTER_RB": "1"},
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "0"},                      # every item: exact fallback
     {"LSAPGPU_SCAN_FILTER": "2", "LSAPGPU_FILTER_QUEUE": "3"},                      # frequent overflow
 ])
@@ -91,7 +93,7 @@ def test_filter_is_the_default_long_row_scan(gpu_ctx):
     """fp32 rows too long for the resident kernel take the filter kernel."""
     gpu_ctx.generate("f32", 12000, 1)
     plan = gpu_ctx.scan_plan()
-    assert plan["filter"] == 16 and plan["m"] == 2, plan
+    assert plan["filter"] == 16 and plan["m"] == 2 and plan["filter_tmem"] == 1, plan
 
 
 def test_filter_after_storage_misspeculation(gpu_ctx):
@@ -142,6 +144,7 @@ def _large(n, env):
     (100000, {}),                                                      # C5 plan: int8 copies, 1 row buffer, 8 slots
     (100000, {"LSAPGPU_FILTER_QUEUE": "512"}),
     (60000, {"LSAPGPU_FILTER_BITS": "8"}),
+    (60000, {"LSAPGPU_FILTER_TMEM": "0"}),                              # (default: 15 chunks of aux in TMEM)
     (100000, {"LSAPGPU_FILTER_CHECK": "7"}),                           # every 7th item re-verified unfiltered
 ])
 def test_filter_large_n_deterministic_and_exact(n, env):
