@@ -201,8 +201,9 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
           p.max_segments = 1;
           p.l2_prefetch = 0;
           p.filter_queue = qcap;
-          // aux[] in tensor memory: 32 * chunks columns of 512 (n <= 65536)
-          p.filter_tmem = tmem_aux && (d.n + chunk - 1) / chunk <= 16 ? 1 : 0;
+          // aux[] in tensor memory: the first 16 chunks (512 columns; all of
+          // it for n <= 65536), the rest from L2
+          p.filter_tmem = tmem_aux;
           done = true;
           break;
         }

@@ -84,10 +84,12 @@ __device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, uint32_t dep) {
       : "memory");
 }
 
-// Tensor memory (TMEM) holding the launch's aux[] words when they fit (C4):
-// consumer warp w keeps the words of its positions in TMEM lane quarter w % 4,
-// columns (w / 4) * nch * V + c * V .. + V - 1 for chunk c, and reads a
-// chunk's V words with one 32x32b load instead of V / 4 L2 loads per item.
+// Tensor memory (TMEM) holding the launch's aux[] words: consumer warp w
+// keeps the words of its positions in TMEM lane quarter w % 4, columns
+// (w / 4) * ntm * V + c * V .. + V - 1 for chunk c < ntm = min(chunks, 16)
+// (512 columns), and reads a chunk's V words with one 32x32b load instead of
+// V / 4 L2 loads per item; chunks beyond the first 16 (n > 65536) still come
+// from L2.
 __device__ __forceinline__ void tmem_alloc512(uint32_t* dst_smem) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst_smem))
                : "memory");
@@ -229,14 +231,15 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
   }
   __syncthreads();
   uint32_t tmem_base = 0;
+  const int32_t ntm = kTM ? min(nch, 512 / (4 * kFV)) : 0;  // chunks whose aux lives in TMEM
   if constexpr (kTM) {
     tmem_fence_after();
     tmem_base = tmem_base_s;
     if (warp < kFW) {  // each consumer warp stores the aux words of its own positions, every chunk
       const int32_t lo0 = warp * kFBlk + lane * kFV;
       const uint32_t tw = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                          static_cast<uint32_t>((warp >> 2) * nch * kFV);
-      for (int32_t c = 0; c < nch; ++c) {
+                          static_cast<uint32_t>((warp >> 2) * ntm * kFV);
+      for (int32_t c = 0; c < ntm; ++c) {
         const int64_t p = static_cast<int64_t>(c) * kFChunk + lo0;
         AuxW<kFV> x;
         ld_aux<kFV>(x, aux_g + p, p < n);
@@ -502,12 +505,11 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
     // chunk's compute (long-scoreboard stalls with a one-chunk lead)
     AuxW<kFV> nx, fx;
     int32_t cnext = nch > 1 ? 1 : 0;  // chunk held in fx
-    if constexpr (!kTM) {
-      load_aux(0, nx);
-      load_aux(cnext, fx);
-    }
+    const bool all_tm = kTM && ntm == nch;  // (otherwise chunks >= ntm rotate through nx / fx as below)
+    if (0 >= ntm) load_aux(0, nx);
+    if (cnext >= ntm) load_aux(cnext, fx);
     const uint32_t tw = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                        static_cast<uint32_t>((warp >> 2) * nch * kFV);
+                        static_cast<uint32_t>((warp >> 2) * ntm * kFV);
     for (int32_t q = 0; q < stages; ++q) {
       const int rb = q % RB;
       const int par = q & 1;
@@ -519,16 +521,18 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
       int32_t tshare = kFNeg;  // last read of tmax[par]
       for (int32_t c = 0; c < nch; ++c) {
         AuxW<kFV> ax;
-        if constexpr (kTM) {
+        const bool in_tm = c < ntm;  // (warp-uniform)
+        if (in_tm)
           tmem_ld8(tw + static_cast<uint32_t>(c * kFV), ax.w);  // completes behind the slot wait
-        } else {
+        else
           ax = nx;
+        if (!all_tm) {
           nx = fx;
           cnext = cnext + 1 < nch ? cnext + 1 : 0;  // chunk c + 2 (wrapping into the next item)
-          load_aux(cnext, fx);
+          if (cnext >= ntm) load_aux(cnext, fx);
         }
         mbar_wait_backoff(&slot_full[s], fph, 20);
-        if constexpr (kTM) tmem_wait_ld();
+        if (in_tm) tmem_wait_ld();
         const unsigned char* sb = slots + s * kSlotBytes;
         const uint4 qv = lds_q<Q, kFV>(sb + lo * static_cast<int>(sizeof(Q)));
         const uint32_t(&aw)[kFV] = ax.w;

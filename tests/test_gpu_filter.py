@@ -143,6 +143,7 @@ def _large(n, env):
 @pytest.mark.parametrize("n,env", [
     (100000, {}),                                                      # C5 plan: int8 copies, 1 row buffer, 8 slots
     (100000, {"LSAPGPU_FILTER_QUEUE": "512"}),
+    (100000, {"LSAPGPU_FILTER_TMEM": "0"}),                             # (default: 16 of 25 aux chunks in TMEM)
     (60000, {"LSAPGPU_FILTER_BITS": "8"}),
     (60000, {"LSAPGPU_FILTER_TMEM": "0"}),                              # (default: 15 chunks of aux in TMEM)
     (100000, {"LSAPGPU_FILTER_CHECK": "7"}),                           # every 7th item re-verified unfiltered
