@@ -153,9 +153,12 @@ __device__ __forceinline__ uint4 lds_q(const unsigned char* p) {
   }
 }
 
-template <class E, class Q, int RB, int W, int V, bool kTM>
+// kAux: 0 = aux[] from L2, 1 = the first 16 chunks from TMEM and the rest
+// from L2, 2 = every chunk from TMEM (n <= 65536: no L2 lookahead code at all)
+template <class E, class Q, int RB, int W, int V, int kAux>
 __global__ void __launch_bounds__(32 * (W + 3), 1)
     pair_scan_filter_kernel(DevState st, int full, int NS, int qcap) {
+  constexpr bool kTM = kAux > 0, kAllTM = kAux == 2;
   static_assert(!kTM || V == 8, "TMEM aux: 8 words per lane per chunk");
   // the geometry of this instantiation (shadowing the default constants)
   constexpr int kFW = W;
@@ -505,9 +508,11 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
     // chunk's compute (long-scoreboard stalls with a one-chunk lead)
     AuxW<kFV> nx, fx;
     int32_t cnext = nch > 1 ? 1 : 0;  // chunk held in fx
-    const bool all_tm = kTM && ntm == nch;  // (otherwise chunks >= ntm rotate through nx / fx as below)
-    if (0 >= ntm) load_aux(0, nx);
-    if (cnext >= ntm) load_aux(cnext, fx);
+    // (chunks >= ntm rotate through nx / fx, two chunks ahead)
+    if constexpr (!kAllTM) {
+      if (0 >= ntm) load_aux(0, nx);
+      if (cnext >= ntm) load_aux(cnext, fx);
+    }
     const uint32_t tw = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                         static_cast<uint32_t>((warp >> 2) * ntm * kFV);
     for (int32_t q = 0; q < stages; ++q) {
@@ -521,12 +526,12 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
       int32_t tshare = kFNeg;  // last read of tmax[par]
       for (int32_t c = 0; c < nch; ++c) {
         AuxW<kFV> ax;
-        const bool in_tm = c < ntm;  // (warp-uniform)
+        const bool in_tm = kAllTM || c < ntm;  // (warp-uniform)
         if (in_tm)
           tmem_ld8(tw + static_cast<uint32_t>(c * kFV), ax.w);  // completes behind the slot wait
         else
           ax = nx;
-        if (!all_tm) {
+        if constexpr (!kAllTM) {
           nx = fx;
           cnext = cnext + 1 < nch ? cnext + 1 : 0;  // chunk c + 2 (wrapping into the next item)
           if (cnext >= ntm) load_aux(cnext, fx);
@@ -631,11 +636,11 @@ __global__ void filter_aux_kernel(DevState st) {
   }
 }
 
-template <class E, class Q, int RB, int W, int V, bool kTM>
+template <class E, class Q, int RB, int W, int V, int kAux>
 cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
   cudaError_t e = launch_pdl(filter_aux_kernel<E, Q>, dim3(p.ctas), dim3(256), 0, st, d.pdl, d);
   if (e != cudaSuccess) return e;
-  auto k = pair_scan_filter_kernel<E, Q, RB, W, V, kTM>;
+  auto k = pair_scan_filter_kernel<E, Q, RB, W, V, kAux>;
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
   if (e != cudaSuccess) return e;
   return launch_pdl(k, dim3(p.ctas), dim3(32 * (W + 3)), p.smem, st, d.pdl, d, full, p.bufs, p.filter_queue);
@@ -647,8 +652,9 @@ cudaError_t launch_filter_t(const DevState& d, const ScanPlan& p, int full, cuda
 // instead of the copy per chunk 6-17% slower: a later aux load issue)
 template <class E, class Q, int RB>
 cudaError_t launch_filter_g(const DevState& d, const ScanPlan& p, int full, cudaStream_t st) {
-  if (p.filter_tmem) return launch_filter_t<E, Q, RB, 16, 8, true>(d, p, full, st);
-  return launch_filter_t<E, Q, RB, 16, 8, false>(d, p, full, st);
+  if (p.filter_tmem && (d.n + 4095) / 4096 <= 16) return launch_filter_t<E, Q, RB, 16, 8, 2>(d, p, full, st);
+  if (p.filter_tmem) return launch_filter_t<E, Q, RB, 16, 8, 1>(d, p, full, st);
+  return launch_filter_t<E, Q, RB, 16, 8, 0>(d, p, full, st);
 }
 
 }  // namespace scan_detail
