@@ -282,7 +282,8 @@ int lsapgpu_scan_timing(const lsapgpu_ctx* ctx, double* total_ms, int64_t* launc
 /* The pair-scan plan chosen for the current matrix (instrumentation): up to
  * cap of {kernel (0 streaming, 1 resident, 2 quantized filter), items or row
  * buffers per CTA, stage buffers or chunk slots, filter bits (0, 8, 16), CTAs,
- * threads per CTA, dynamic smem bytes, chunk, filter queue capacity}.
+ * threads per CTA, dynamic smem bytes, chunk, filter queue capacity, filter
+ * aux in tensor memory (0 / 1)}.
  * Returns the number of values written, < 0 on error. */
 int lsapgpu_scan_plan(const lsapgpu_ctx* ctx, int32_t* info, int32_t cap);
 
