@@ -343,6 +343,10 @@ int ensure_vectors(lsapgpu_ctx* ctx, int32_t n) {
   CK(valloc(ctx, &d.items_own, N, false));
   CK(valloc(ctx, &d.aux, N, true));
   d.log_cap = std::max<int64_t>(1 << 20, 8 * static_cast<int64_t>(n));
+  // (tests: LSAPGPU_LOG_CAP shrinks the delta log so a pass drains it; a batch
+  // appends at most 2n entries, so the cap never goes below that)
+  if (const char* e = std::getenv("LSAPGPU_LOG_CAP"))
+    d.log_cap = std::max<int64_t>(std::atoll(e), 2 * static_cast<int64_t>(n) + 64);
   CK(valloc(ctx, &d.log, static_cast<size_t>(d.log_cap), false));
   CK(valloc(ctx, &d.log_sorted, static_cast<size_t>(d.log_cap), false));
   d.part_cap = (static_cast<int64_t>(n) + 8) * 16;

@@ -145,3 +145,39 @@ def test_device_log_order_equals_host_order():
     assert all(v[3] == 0 for v in dev.values()), dev
     assert all(v[3] > 0 for v in host.values()), host
     assert {k: v[:3] for k, v in dev.items()} == {k: v[:3] for k, v in host.items()}
+
+
+DRAIN_CASE = r'''
+import sys, json, hashlib; sys.path.insert(0, %r)
+import paper_1106_5694_b200 as g
+ctx = g.Context(0)
+out = {}
+for kind, n in (("p2p", 2000), ("f32", 1500)):
+    ctx.generate(kind, n, 2)
+    for graph in (True, False):
+        for trace in (True, False):
+            r = ctx.solve(g.ParallelConfig(seed=5, use_graph=graph), trace=trace)
+            out["%%s-%%d-%%d" %% (kind, graph, trace)] = [float(r.assignment.value).hex(), r.switches_applied,
+                hashlib.sha256(r.assignment.sigma.tobytes()).hexdigest(), r.outer_iterations,
+                hashlib.sha256(repr(list(r.objective_trace)).encode()).hexdigest()]
+print(json.dumps(out))
+'''
+
+
+def test_delta_log_drain_mid_pass():
+    """A pass whose exchanges overflow the delta log drains it to the host and
+    continues the inner loop (parallel.cpp has no such limit; the replay must
+    not notice): with the log capped at ~2n entries (LSAPGPU_LOG_CAP) every
+    solve -- graph / host-stepped, trace on / off, integer and fp32 storage --
+    equals the uncapped one bit for bit, trace included."""
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(env):
+        r = subprocess.run([sys.executable, "-c", DRAIN_CASE % root], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+
+    base, capped = run({}), run({"LSAPGPU_LOG_CAP": "1"})
+    assert base == capped
