@@ -658,7 +658,26 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   int64_t chunk_rows = static_cast<int64_t>(chunk_src / (static_cast<size_t>(n) * 8)) / 32 * 32;
   if (chunk_rows < 32) chunk_rows = 32;
   if (chunk_rows > n) chunk_rows = n;
-  const int nchunks = static_cast<int>((n + chunk_rows - 1) / chunk_rows);
+  // Chunk row ranges: full chunks, except that the last full chunk's rows go
+  // out as four quarter chunks -- the copy and layout pass after the last
+  // host slice are on the critical path, so the final piece is kept small.
+  std::vector<int64_t> cstart;
+  for (int64_t r = 0; r < n; r += chunk_rows) cstart.push_back(r);
+  if (cstart.size() >= 2 && chunk_rows >= 128) {
+    const int64_t last = cstart.back(), q = chunk_rows / 4 / 32 * 32;
+    if (n - last >= chunk_rows / 2) {  // a large last chunk: quarter it
+      cstart.pop_back();
+      for (int64_t k = 0; k < 4 && last + k * q < n; ++k) cstart.push_back(last + k * q);
+    } else {  // a small remainder: quarter the full chunk before it
+      const int64_t r0 = last - chunk_rows;
+      cstart.pop_back();
+      cstart.pop_back();
+      for (int64_t k = 0; k < 4; ++k) cstart.push_back(r0 + k * q);
+      cstart.push_back(last);
+    }
+  }
+  const int nchunks = static_cast<int>(cstart.size());
+  cstart.push_back(n);
   if (static_cast<int>(ctx->chunk_flags_cap) < nchunks) {
     if (ctx->chunk_flags) cudaFree(ctx->chunk_flags);
     ctx->chunk_flags = nullptr;
@@ -715,8 +734,8 @@ int upload_narrow(lsapgpu_ctx* ctx, const double* data, int32_t n, int storage, 
   ctx->pool->run([&](int t) {
     if (t) cudaSetDevice(device);  // ring events are waited on, and chunks enqueued, from every thread
     for (int k = 0; k < nchunks && !stop.load(std::memory_order_relaxed); ++k) {
-      const int64_t r0 = static_cast<int64_t>(k) * chunk_rows;
-      const int64_t rows = std::min<int64_t>(chunk_rows, n - r0);
+      const int64_t r0 = cstart[static_cast<size_t>(k)];
+      const int64_t rows = cstart[static_cast<size_t>(k) + 1] - r0;
       const size_t cnt = static_cast<size_t>(rows) * static_cast<size_t>(n);
       const int b = k % kRingNarrow;
       const double tw0 = host_timing ? now_us() : 0.0;
