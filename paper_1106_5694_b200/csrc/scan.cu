@@ -149,7 +149,10 @@ ScanPlan plan_scan(const DevState& d, int num_sms) {
       // (even lists shorter than the grid), so it is opt-in
       p.max_segments = 1;
       if (const char* sg = std::getenv("LSAPGPU_SCAN_SEGMENTS")) p.max_segments = std::atoi(sg);
-      p.l2_prefetch = 0;  // measured slower at every distance (tools/ab.py)
+      // L2 prefetch of the rows one stage ahead: C3 (n = 10k) solve -1.6 %, but
+      // +0.9 % at n = 5k and neutral at 1k (tools/ab.py, round 2): rows of
+      // 16 KB and up only; distance 2 -0.8 %, 4 +8 % at C3
+      p.l2_prefetch = d.n >= 8192 ? 1 : 0;
       if (const char* pf = std::getenv("LSAPGPU_SCAN_L2PF")) p.l2_prefetch = std::atoi(pf);
       if (p.l2_prefetch >= 32 / m) p.l2_prefetch = 32 / m - 1;
     }
