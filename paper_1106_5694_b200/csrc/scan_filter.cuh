@@ -31,10 +31,11 @@
 // Data movement per item: the Q row (gathered at random t: staged in shared
 // memory by TMA) and the QT row (streamed through a ring of TMA chunk slots)
 // -- 2 n sizeof(Q) bytes of HBM instead of 2 n sizeof(float) -- plus aux[]
-// (4 n bytes, L2-resident, shared by every item of the launch), which the
-// consumers load straight into registers (through shared memory it cost as
-// much smem bandwidth as the gather).  Row buffers are double-buffered where
-// two fit.
+// (4 n bytes, shared by every item of the launch), which each CTA copies
+// into its tensor memory once per launch (the first 16 chunks; the rest, for
+// n > 65536, is loaded from L2 straight into registers: through shared
+// memory it cost as much smem bandwidth as the gather).  Row buffers are
+// double-buffered where two fit.
 //
 // Warps: 16 consumers (each takes one 256-position block of every chunk),
 // one row producer, one chunk producer, one verifier that evaluates item q's
@@ -494,9 +495,9 @@ __global__ void __launch_bounds__(32 * (W + 3), 1)
     }
   } else {
     // ---------------- consumers: block `warp` of every chunk ----------------
-    // The 8 aux words of a lane's positions come straight from L2 (aux is
-    // the same for every item of the launch), one chunk ahead in registers;
-    // only the QT chunk and the gathered Q row go through shared memory.
+    // The 8 aux words of a lane's positions come from tensor memory (or, past
+    // the first 16 chunks, from L2 two chunks ahead in registers); only the
+    // QT chunk and the gathered Q row go through shared memory.
     const int32_t lo = warp * kFBlk + lane * kFV;  // position offset within a chunk
     int s = 0;
     uint32_t fph = 0;  // slot_full phase parity
