@@ -517,3 +517,17 @@ def test_trace_buffers_not_shared_between_live_reports(gpu_ctx):
     r3 = gpu_ctx.solve(g.ParallelConfig(seed=3))  # may reuse r2's arrays
     assert list(r1.objective_trace) == t1
     assert list(r3.objective_trace)[0][0] == 0
+
+
+@pytest.mark.parametrize("n", [8192, 9001, 12000, 16000])
+def test_resident_scan_with_l2_prefetch_rows(oracle, gpu_ctx, n):
+    """Resident plans for n >= 8192 prefetch the next stage's rows into L2
+    (M = 2 up to ~10.4k int16 columns, M = 1 above): the records still equal
+    the oracle's bit for bit, incl. ragged n and the packed-key limit 16384."""
+    a = oracle.generate("int", n, 5, 30000.0)
+    gpu_ctx.set_matrix(a)
+    plan = gpu_ctx.scan_plan()
+    assert gpu_ctx.storage == "int16" and plan["kernel"] == "resident", plan
+    sigma = oracle.random_perm(n, 9)
+    assert tables_equal(gpu_ctx.evaluate_all(sigma), *oracle.evaluate_all(a, sigma))
+    assert tables_equal(gpu_ctx.evaluate_all(sigma, 7.0), *oracle.evaluate_all(a, sigma, 7.0))
