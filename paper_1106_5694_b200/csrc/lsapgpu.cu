@@ -171,6 +171,10 @@ struct lsapgpu_ctx {
   Buf qmat;               // Q and QT: quantized filter copies (scan_filter.cuh), when the plan uses them
   int32_t place_rank = 0, place_world = 1;  // row-block placement of A (lsapgpu_set_placement)
   int quant_bits = 0;     // copies the last layout pass wrote (0: none) and their scale
+  // storage of the last device-source matrix (and its n): a repeated upload
+  // of the same shape speculates it without the probe's round trip
+  int last_dev_storage = -1;
+  int32_t last_dev_n = 0;
   double quant_scale = 0.0;
   bool quant_fused = false;  // the current copies came from the layout pass (no quantize pass)
   std::set<const void*> peer_poisoned;  // peer-transport flag arrays whose epochs a failed solve desynchronised
@@ -552,15 +556,25 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
   if (rc) return rc;
   ctx->n_matrix = 0;
   CK(cudaMemsetAsync(ctx->flags_dev, 0, 4 * sizeof(uint32_t), ctx->stream));
-  const int64_t probe = std::min<int64_t>(64, n);
-  CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream, ctx->flags_dev + 3));
-  ++ctx->launches;
   uint32_t fl4[4] = {};
-  CK(cpy(ctx, fl4, ctx->flags_dev, sizeof(fl4), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  uint32_t flags = fl4[0];
-  if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
-  const int spec = storage_of_flags(flags);
+  uint32_t flags = 0;
+  int spec;
+  // Same n as the last device matrix, whose plan built no filter copies (so
+  // no probe max is needed): speculate its storage and skip the probe's
+  // sync; the layout pass's flags decide as always (a wrong guess rebuilds).
+  if (ctx->last_dev_n == n && ctx->last_dev_storage >= 0 && !ctx->scan_plan.filter && ctx->place_world <= 1) {
+    spec = ctx->last_dev_storage;
+  } else {
+    const int64_t probe = std::min<int64_t>(64, n);
+    CK(launch_classify(src, n, 0, probe, ctx->flags_dev, ctx->stream, ctx->flags_dev + 3));
+    ++ctx->launches;
+    CK(cpy(ctx, fl4, ctx->flags_dev, sizeof(fl4), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    flags = fl4[0];
+    if (flags & 1u) return fail(ctx, LSAPGPU_ERR_INVALID, "benefit matrix contains a non-finite entry");
+    spec = storage_of_flags(flags);
+  }
+  ctx->last_dev_storage = -1;  // (set again once this matrix is complete)
   if ((rc = alloc_matrix(ctx, n, spec))) return rc;
   set_source_rows(ctx, &src);
   DevState& d = ctx->d;
@@ -582,7 +596,12 @@ int build_from_source(lsapgpu_ctx* ctx, LayoutSource src, int32_t n) {
     ++ctx->launches;
     CK(cudaStreamSynchronize(ctx->stream));
   }
-  return finish_matrix(ctx, n);
+  const int frc = finish_matrix(ctx, n);
+  if (frc == LSAPGPU_OK) {
+    ctx->last_dev_storage = storage;
+    ctx->last_dev_n = n;
+  }
+  return frc;
 }
 
 // Host upload (lsapgpu_set_matrix): the matrix crosses PCIe in row chunks

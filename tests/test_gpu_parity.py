@@ -531,3 +531,30 @@ def test_resident_scan_with_l2_prefetch_rows(oracle, gpu_ctx, n):
     sigma = oracle.random_perm(n, 9)
     assert tables_equal(gpu_ctx.evaluate_all(sigma), *oracle.evaluate_all(a, sigma))
     assert tables_equal(gpu_ctx.evaluate_all(sigma, 7.0), *oracle.evaluate_all(a, sigma, 7.0))
+
+
+def test_repeated_device_upload_storage_changes(oracle, gpu_ctx):
+    """A repeated device upload of the same n speculates the previous
+    matrix's storage without the probe; every storage change in either
+    direction (narrower, wider, non-finite) is still caught and rebuilt."""
+    import torch
+    n = 700
+    rng = np.random.default_rng(3)
+    sigma = oracle.random_perm(n, 4)
+    seq = [("int16", rng.integers(0, 3000, (n, n)).astype(np.float64)),
+           ("int16", rng.integers(-3000, 0, (n, n)).astype(np.float64)),
+           ("fp64", rng.random((n, n))),
+           ("int16", rng.integers(0, 30000, (n, n)).astype(np.float64)),
+           ("int32", rng.integers(0, 3000000, (n, n)).astype(np.float64)),
+           ("fp32", np.asarray(rng.random((n, n)), np.float32).astype(np.float64)),
+           ("fp32", np.asarray(rng.random((n, n)), np.float32).astype(np.float64))]
+    for storage, a in seq:
+        gpu_ctx.set_matrix(torch.from_numpy(a).cuda())
+        assert gpu_ctx.storage == storage
+        assert tables_equal(gpu_ctx.evaluate_all(sigma), *oracle.evaluate_all(a, sigma)), storage
+    bad = seq[-1][1].copy()
+    bad[-1, -1] = np.inf
+    with pytest.raises(Exception, match="non-finite"):
+        gpu_ctx.set_matrix(torch.from_numpy(bad).cuda())
+    gpu_ctx.set_matrix(torch.from_numpy(seq[0][1]).cuda())  # usable again after the error
+    assert gpu_ctx.storage == "int16"
